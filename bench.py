@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark: PRN x Doppler acquisition cells/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c3] [--impl ours|reference]
+
+A *cell* is one (snapshot, PRN, Doppler bin) searched over all code phases and all
+noncoherent rounds. One *step* is one full search of the per-GPU
+batch of synthetic snapshots. Snapshots are sharded across ranks (one process per GPU,
+weak scaling: the per-GPU batch is fixed) with no data-path collective; the step time
+is the device timeline of the library's own stream (CUDA events recorded by libgacq
+around each whole gacq_run), max over ranks.
+
+`value`  : batch resident in HBM before the timed region.
+`e2e`    : the public API (AcqEngine.search) on a pinned host batch: H2D of the step's
+           snapshots + search + D2H of the result rows + host metric, wall-clocked.
+`--impl reference` times the CPU path (the pinned oracle restatement of the reference,
+oracle/, scipy.fft) on the host cores with one process per core, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
+UNIT = "cells/s"
+
+# BASELINE.json configs; c3 is the one the metric is quoted on
+CONFIGS = {
+    "c1": dict(fs=4.092e6, rounds=1, step=500.0, span_hz=5000.0, batch=1024,
+               desc="C1: 1 ms snapshots @4.092 MHz, 32 PRNs x 21 bins (+-5 kHz/500 Hz), 1 x 1 ms"),
+    "c2": dict(fs=4.092e6, rounds=10, step=250.0, span_hz=5000.0, batch=512,
+               desc="C2: 10 ms snapshots @4.092 MHz, 32 PRNs x 41 bins (+-5 kHz/250 Hz), 10 x 1 ms noncoherent"),
+    "c3": dict(fs=4.092e6, rounds=10, step=500.0, span_hz=5000.0, batch=1024,
+               desc="C3: 10 ms snapshots @4.092 MHz, 32 PRNs x 21 bins (+-5 kHz/500 Hz), 10 x 1 ms noncoherent"),
+    "c4": dict(fs=16.368e6, rounds=20, step=125.0, span_hz=10000.0, batch=16,
+               desc="C4: 20 ms snapshots @16.368 MHz, 32 PRNs x 161 bins (+-10 kHz/125 Hz), 20 x 1 ms noncoherent"),
+}
+
+
+def acq_kwargs(c):
+    return dict(doppler_min_hz=-c["span_hz"], doppler_max_hz=c["span_hz"], doppler_step_hz=c["step"],
+                noncoherent_rounds=c["rounds"])
+
+
+def flops_per_cell(c, n_bins):
+    """SURVEY.md 8(d) algorithmic FLOPs at the reference's native N (implementation-independent)."""
+    n = round(c["fs"] * 1e-3)
+    p = n
+    corr = c["rounds"] * (6 * n + 5 * n * math.log2(n) + 3 * p + p)
+    fwd = c["rounds"] * (6 * n + 5 * n * math.log2(n)) / 32
+    return corr, fwd
+
+
+def bytes_per_cell(c, n_bins):
+    n = round(c["fs"] * 1e-3)
+    return 8 * n * c["rounds"] / (32 * n_bins) + 16 / n_bins
+
+
+# ------------------------------------------------------------------ CPU (oracle) legs
+def _cpu_worker_init():
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, str(ROOT))
+
+
+def _cpu_warm(cname):
+    import oracle
+
+    c = CONFIGS[cname]
+    x, _ = oracle.make_snapshot(0, c["fs"], c["rounds"] * 1e-3, base_seed=1)
+    oracle.acquire_all(x[: round(c["fs"] * 1e-3) * 1], c["fs"], range(1, 33),
+                       oracle.OracleConfig(**{**acq_kwargs(c), "noncoherent_rounds": 1}))
+    return os.getpid()
+
+
+def _cpu_one(arg):
+    import oracle
+
+    cname, x = arg
+    c = CONFIGS[cname]
+    return len(oracle.acquire_all(x, c["fs"], range(1, 33), oracle.OracleConfig(**acq_kwargs(c))))
+
+
+def cpu_measure(cname, workers, steps, warmup, per_worker=1):
+    """Oracle (restatement of acquisition.py:112-170 on scipy.fft) on `workers` processes,
+    one snapshot per worker per step; returns (cells/s per step list, sample description)."""
+    import oracle
+
+    c = CONFIGS[cname]
+    n_bins = oracle.OracleConfig(**acq_kwargs(c)).doppler_bins_hz().size
+    n = workers * per_worker
+    snaps = [oracle.make_snapshot(i, c["fs"], c["rounds"] * 1e-3, base_seed=900)[0] for i in range(n)]
+    ctx = mp.get_context("spawn")
+    rates = []
+    with ctx.Pool(workers, initializer=_cpu_worker_init) as pool:
+        pool.map(_cpu_warm, [cname] * workers, chunksize=1)
+        for it in range(warmup + steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_one, [(cname, s) for s in snaps], chunksize=1)
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                rates.append(n * 32 * n_bins / dt)
+    sample = (f"{n} {cname.upper()} snapshots x 32 PRNs x {n_bins} bins per step, {workers} processes "
+              f"(oracle/ restatement of acquisition.py:112-170, scipy {__import__('scipy').__version__} fft)")
+    return rates, sample
+
+
+# ------------------------------------------------------------------ GPU helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def synth_batch(torch, n, c, seed, device):
+    """Synthetic GPS-like snapshots on the GPU: 8 visible satellites (random PRN, Doppler
+    U(-4750,4750), integer code phase, carrier phase, C/N0 U(38,48) dB-Hz) + AWGN at the
+    45 dB-Hz reference level. Perf input only (parity uses the oracle's synthesis)."""
+    from paper_1309_0052_b200 import generate_ca_code
+
+    fs = c["fs"]
+    d = round(fs / 1.023e6)
+    span = round(fs * 1e-3) * c["rounds"]
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    chips = torch.tensor(np.stack([generate_ca_code(p).chips for p in range(1, 33)]),
+                         dtype=torch.float32, device=device)
+    out = torch.empty((n, span), dtype=torch.complex64, device=device)
+    idx = torch.arange(span, device=device, dtype=torch.int64)
+    sigma = math.sqrt(fs / (2.0 * 10.0 ** (45.0 / 10.0)))
+    chunk = 32
+    for s0 in range(0, n, chunk):
+        m = min(chunk, n - s0)
+        noise = torch.randn((m, span, 2), generator=g, device=device) * sigma
+        x = torch.view_as_complex(noise.contiguous())
+        for _ in range(8):
+            prn = torch.randint(0, 32, (m,), generator=g, device=device)
+            dop = (torch.rand((m,), generator=g, device=device, dtype=torch.float64) * 2 - 1) * (c["span_hz"] - 250)
+            cph = torch.randint(0, 1023 * d, (m,), generator=g, device=device)
+            carr = torch.rand((m,), generator=g, device=device, dtype=torch.float64)
+            cn0 = 38.0 + 10.0 * torch.rand((m,), generator=g, device=device, dtype=torch.float64)
+            amp = (10.0 ** ((cn0 - 45.0) / 20.0)).to(torch.float32)
+            ci = torch.div(idx[None, :] - cph[:, None], d, rounding_mode="floor").remainder(1023)
+            code = chips[prn[:, None], ci]
+            ph = torch.frac(dop[:, None] * idx[None, :].double() / fs + carr[:, None]) * (2 * math.pi)
+            x += (amp[:, None] * code) * torch.polar(torch.ones_like(ph, dtype=torch.float32), ph.float())
+        out[s0:s0 + m] = x
+    return out
+
+
+# ------------------------------------------------------------------ arms
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    rates, sample = cpu_measure(args.config, cores, args.steps, args.warmup)
+    v = statistics.mean(rates)
+    c = CONFIGS[args.config]
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic (oracle.make_snapshot)",
+            "impl": "reference",
+            "config": {"workload": c["desc"], "parallelism": f"{cores} CPU processes"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    c = CONFIGS[args.config]
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = max(1, min(os.cpu_count() or 1, 16))
+        rates, sample = cpu_measure(args.config, workers, 1, 0)
+        cpu_baseline = {"value": rates[0], "unit": UNIT, "cores": workers, "kind": "port", "sample": sample}
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import paper_1309_0052_b200 as g
+
+    cfg = g.AcqConfig(**acq_kwargs(c))
+    n_bins = cfg.doppler_bins_hz().size
+    batch = args.batch or c["batch"]
+    eng = g.AcqEngine(c["fs"], list(range(1, 33)), cfg, device=local_rank)
+    dev = synth_batch(torch, batch, c, seed=1000 + rank, device=torch.device("cuda", local_rank))
+    pinned = g.PinnedBuffer(tuple(dev.shape))
+    pinned.array[...] = dev.cpu().numpy()
+    torch.cuda.synchronize()
+    in_bytes = dev.numel() * 8
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.run_rows(dev)
+    barrier()
+    props = torch.cuda.get_device_properties(local_rank)
+    gpu_id = getattr(props, "pci_bus_id", None) or str(local_rank)
+    if isinstance(gpu_id, int):
+        gpu_id = str(local_rank)
+    eng.reset_stats()
+    t_wall = time.perf_counter()
+    with ClockSampler(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank]
+                      if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local_rank)) as clk:
+        for _ in range(args.steps):
+            rows = eng.run_rows(dev, profile=True)
+        torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    barrier()
+    st = eng.stats()
+    dev_ms = st["run_ms"]
+    if dist:
+        t = torch.tensor([dev_ms, t_wall], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, t_wall_max = float(t[0]), float(t[1])
+    else:
+        t_wall_max = t_wall
+    cells_step = batch * 32 * n_bins
+    value = world * cells_step * args.steps / (dev_ms / 1e3)
+
+    # e2e through the public API from pinned host memory
+    eng.search(pinned.array)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = eng.search(pinned.array)
+        _ = int(res.detected.sum())
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e_value = world * cells_step * args.steps / e2e_s
+
+    f_corr, f_fwd = flops_per_cell(c, n_bins)
+    sm = props.multi_processor_count
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    max_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = sm * 128 * 2 * max_mhz * 1e6 / 1e12
+    corr_s = st["corr_ms"] / 1e3
+    achieved = st["cells"] * f_corr / corr_s / 1e12 if corr_s > 0 else None
+    traffic = None
+    prof = ROOT / "profiles" / "corr_traffic.json"
+    cells_per_launch = st["cells"] / max(1, st["corr_launches"])
+    if prof.exists():
+        pj = json.loads(prof.read_text())
+        if pj.get("config") == args.config and pj.get("dram_bytes_per_cell"):
+            traffic = pj["dram_bytes_per_cell"] * cells_per_launch
+    hbm = float(peaks.get("hbm_gbs", 6547.8))
+    step_cells_s = cells_step * args.steps / (dev_ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (8 satellites + AWGN per snapshot, generated on device)",
+        "config": {"workload": c["desc"], "snapshots_per_gpu": batch, "global_batch": batch * world,
+                   "cells_per_step_per_gpu": cells_step, "fs_hz": c["fs"], "prns": 32, "bins": n_bins,
+                   "parallelism": f"dp{world} (snapshot shards, no collective)",
+                   "l2": f"inputs larger than L2 ({in_bytes / 2**20:.0f} MiB per GPU), no flush"},
+        "roofline": {"bound": "fp32", "kernel": "gacq_corr_kernel", "achieved": achieved, "peak": fp32_peak,
+                     "unit": "TFLOP/s", "frac": achieved / fp32_peak if achieved else None,
+                     "traffic": traffic,
+                     "peak_source": f"nominal FP32 {sm} SMs x 128 lanes x 2 x {max_mhz:.0f} MHz "
+                                    "(MEASURED_PEAKS.json has no FP32 entry)",
+                     "flops_per_cell": f_corr,
+                     "cells_per_launch": cells_per_launch,
+                     "avg_launch_ms": st["corr_ms"] / max(1, st["corr_launches"]),
+                     "step_frac": step_cells_s * (f_corr + f_fwd) / 1e12 / fp32_peak},
+        "roofline_hbm": {"achieved": step_cells_s * bytes_per_cell(c, n_bins) / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": step_cells_s * bytes_per_cell(c, n_bins) / 1e9 / hbm,
+                         "note": "compulsory bytes/cell (SURVEY 8(d)); the path is FP32-bound"},
+        "kernel_ms": {"fwd": st["fwd_ms"] / args.steps, "corr": st["corr_ms"] / args.steps,
+                      "reduce": st["reduce_ms"] / args.steps},
+        "cpu_baseline": cpu_baseline,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
+                "d2h_bytes_per_step": batch * 32 * 16, "api": "AcqEngine.search(pinned host batch)"},
+        "gpu_launches": st["launches"],
+        "wall_ms_per_step": t_wall_max * 1e3 / args.steps,
+        "clocks": clk.summary(),
+        "detected_per_snapshot": float(rows.shape[0] and eng.finish(rows).detected.sum() / rows.shape[0]),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    pinned.close()
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="snapshots per GPU (default: config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * gacq.h -- C ABI of the B200-native GPS L1 C/A acquisition engine (libgacq.so).
+ *
+ * Drop-in boundary for the reference's acquisition hot path
+ * (gnssperf, /root/reference/pkg/src/gnssperf):
+ *
+ *   gacq_create        replaces the per-(prn, fs, n, precision) conjugate code-spectrum
+ *                      cache (acquisition.py:84-105) and the per-bin carrier replicas
+ *                      (acquisition.py:139 -> gnss_signal.py:49-72 -> kernels.py:106-114,
+ *                      175-185): all tables are built once per plan and kept in HBM.
+ *   gacq_run           replaces acquire_all / acquire_channel (acquisition.py:112-208)
+ *                      over a batch of snapshots: the hot loop acquisition.py:138-149
+ *                      (wipe-off, FFT, x conj(code FFT), IFFT, |.|^2 noncoherent sum)
+ *                      and the argmax / exclusion-floor reduction acquisition.py:151-159.
+ *                      The host finishes acquisition.py:160-170 (metric = peak/floor in
+ *                      double, detection, AcqResult) exactly as the reference does.
+ *   gacq_ca_code       replaces generate_ca_code (cacode.py:41-58).
+ *
+ * Plain C types only: pointers, sizes, POD structs. All functions return 0 on success
+ * or a negative GACQ_ERR_* code; gacq_last_error() returns the calling thread's message.
+ * A context is bound to one CUDA device; calls on one context are serialized internally,
+ * distinct contexts (one per device) may be driven concurrently from different threads.
+ */
+#ifndef GACQ_H
+#define GACQ_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GACQ_ABI_VERSION 1
+
+#define GACQ_OK 0
+#define GACQ_ERR_INVALID (-1)     /* -> InvalidInputError (errors.py:8-9)            */
+#define GACQ_ERR_UNSUPPORTED (-2) /* configuration outside the GPU path's support     */
+#define GACQ_ERR_CUDA (-3)        /* device / driver failure -> ResourceError          */
+#define GACQ_ERR_RESOURCE (-4)    /* allocation failure     -> ResourceError (24-25)   */
+
+/* gacq_run flags */
+#define GACQ_SNAPS_ON_DEVICE 1u /* `snaps` is a device pointer (HBM-resident batch)   */
+#define GACQ_ROWS_ON_DEVICE 2u  /* `rows` is a device pointer (no D2H)                */
+#define GACQ_ROWS_PER_BIN 4u    /* write [n_snap][n_prn][n_bins] rows, no bin merge   */
+#define GACQ_PROFILE 8u         /* time each kernel with CUDA events (gacq_stats)     */
+
+typedef struct gacq_ctx gacq_ctx;
+
+typedef struct gacq_params {
+    double sample_rate_hz;            /* IqBuffer.sample_rate_hz (buffers.py:46-66)       */
+    int32_t coherent_ms;              /* AcqConfig.coherent_ms      (acquisition.py:49)   */
+    int32_t noncoherent_rounds;       /* AcqConfig.noncoherent_rounds (acquisition.py:50) */
+    int32_t n_bins;                   /* len(AcqConfig.doppler_bins_hz())                 */
+    const double* doppler_bins_hz;    /* the float64 grid itself (acquisition.py:68-70)  */
+    int32_t exclusion_radius_samples; /* resolved radius (acquisition.py:155), > 0        */
+    int32_t n_prn;                    /* channels searched per snapshot, 1..32            */
+    const int32_t* prns;              /* PRN numbers 1..32, distinct                      */
+    int32_t device;                   /* CUDA ordinal                                     */
+    int32_t reserved;
+    int64_t scratch_bytes;            /* spectrum scratch budget, 0 = default (1 GiB)     */
+} gacq_params;
+
+/* One reduced search row: the winning (bin, lag) of a (snapshot, prn) -- or of a
+ * (snapshot, prn, bin) with GACQ_ROWS_PER_BIN -- with its float32 power and the float32
+ * exclusion floor of that row (acquisition.py:151-159). 16 bytes. */
+typedef struct gacq_row {
+    int32_t bin;
+    int32_t lag;
+    float peak;
+    float floor;
+} gacq_row;
+
+typedef struct gacq_info {
+    int32_t samples_per_period; /* P  = round(fs*1023/1.023e6) (acquisition.py:108-109) */
+    int32_t n_coh;              /* samples per coherent block  (acquisition.py:116)     */
+    int32_t chip_oversample;    /* D  = P / 1023 samples per chip                       */
+    int32_t fft_len;            /* M  = 2048 transform length on the device             */
+    int32_t n_bins;
+    int32_t n_prn;
+    int32_t rounds;
+    int32_t path;               /* 1 = chip-polyphase 2048-point path                   */
+} gacq_info;
+
+typedef struct gacq_stats {
+    int64_t calls;
+    int64_t launches;           /* kernels launched by gacq_run since the last reset    */
+    int64_t cells;              /* (snapshot, prn, bin) cells searched                 */
+    int64_t h2d_bytes;
+    int64_t d2h_bytes;
+    double fwd_ms;              /* summed kernel times (GACQ_PROFILE runs only)         */
+    double corr_ms;
+    double reduce_ms;
+    int64_t fwd_launches;
+    int64_t corr_launches;
+    int64_t reduce_launches;
+    double run_ms;              /* device timeline of whole gacq_run calls, first H2D (or
+                                   first kernel) to last D2H (GACQ_PROFILE runs only)     */
+} gacq_stats;
+
+int gacq_version(void);
+const char* gacq_last_error(void);
+
+/* Build a search plan on `device`: validates the configuration, builds the carrier
+ * table [n_bins][n_coh] (bit-identical to the reference NCO), the conjugate code spectra
+ * and twiddles, and allocates device scratch. */
+int gacq_create(gacq_ctx** out, const gacq_params* params);
+int gacq_info_get(const gacq_ctx* ctx, gacq_info* out);
+void gacq_destroy(gacq_ctx* ctx);
+
+/* Search n_snap snapshots. Snapshot i starts at complex sample i*stride_samples of
+ * `snaps` (interleaved float32 I/Q, complex64) and must hold >= rounds*n_coh samples;
+ * only the first rounds*n_coh are read (acquisition.py:134-137). `rows` receives
+ * n_snap*n_prn records (or n_snap*n_prn*n_bins with GACQ_ROWS_PER_BIN), ordered like the
+ * plan's PRN list. Blocks until results are in `rows`. */
+int gacq_run(gacq_ctx* ctx, const void* snaps, int64_t n_snap, int64_t stride_samples,
+             uint32_t flags, gacq_row* rows);
+
+/* Debug/parity hook: the float32 noncoherent power map [n_prn][n_bins][P] of ONE host
+ * snapshot (the reference's power_map, acquisition.py:131-149). */
+int gacq_power_map(gacq_ctx* ctx, const void* snap_host, float* out_host);
+
+int gacq_stats_get(const gacq_ctx* ctx, gacq_stats* out);
+int gacq_stats_reset(gacq_ctx* ctx);
+
+/* Page-locked host buffers for overlapped H2D (cudaHostAlloc / cudaFreeHost). */
+int gacq_host_alloc(int64_t bytes, void** out);
+int gacq_host_free(void* ptr);
+
+/* C/A chips (+1/-1) of PRN 1..32 into out[1023] (cacode.py:41-58). */
+int gacq_ca_code(int32_t prn, int8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GACQ_H */

@@ -1,0 +1,94 @@
+"""ctypes binding of libgacq.so (include/gacq.h). No fallback: importing this module
+without the built extension raises."""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import InvalidInputError, ResourceError, UnsupportedError
+
+LIB_PATH = Path(__file__).resolve().parent / "libgacq.so"
+
+OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_CUDA, ERR_RESOURCE = 0, -1, -2, -3, -4
+SNAPS_ON_DEVICE, ROWS_ON_DEVICE, ROWS_PER_BIN, PROFILE = 1, 2, 4, 8
+
+
+class Params(C.Structure):
+    _fields_ = [("sample_rate_hz", C.c_double), ("coherent_ms", C.c_int32),
+                ("noncoherent_rounds", C.c_int32), ("n_bins", C.c_int32),
+                ("doppler_bins_hz", C.POINTER(C.c_double)),
+                ("exclusion_radius_samples", C.c_int32), ("n_prn", C.c_int32),
+                ("prns", C.POINTER(C.c_int32)), ("device", C.c_int32), ("reserved", C.c_int32),
+                ("scratch_bytes", C.c_int64)]
+
+
+class Row(C.Structure):
+    _fields_ = [("bin", C.c_int32), ("lag", C.c_int32), ("peak", C.c_float), ("floor", C.c_float)]
+
+
+class Info(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("samples_per_period", "n_coh", "chip_oversample", "fft_len",
+                                         "n_bins", "n_prn", "rounds", "path")]
+
+
+class Stats(C.Structure):
+    _fields_ = [("calls", C.c_int64), ("launches", C.c_int64), ("cells", C.c_int64),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("fwd_ms", C.c_double),
+                ("corr_ms", C.c_double), ("reduce_ms", C.c_double), ("fwd_launches", C.c_int64),
+                ("corr_launches", C.c_int64), ("reduce_launches", C.c_int64),
+                ("run_ms", C.c_double)]
+
+
+ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
+
+EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
+           "gacq_run", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset", "gacq_host_alloc",
+           "gacq_host_free", "gacq_ca_code")
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_1309_0052_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))  # CDLL releases the GIL for the duration of each call
+    lib.gacq_version.restype = C.c_int
+    lib.gacq_last_error.restype = C.c_char_p
+    lib.gacq_create.argtypes = [C.POINTER(C.c_void_p), C.POINTER(Params)]
+    lib.gacq_info_get.argtypes = [C.c_void_p, C.POINTER(Info)]
+    lib.gacq_destroy.argtypes = [C.c_void_p]
+    lib.gacq_destroy.restype = None
+    lib.gacq_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint32, C.c_void_p]
+    lib.gacq_power_map.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.gacq_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]
+    lib.gacq_stats_reset.argtypes = [C.c_void_p]
+    lib.gacq_host_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
+    lib.gacq_host_free.argtypes = [C.c_void_p]
+    lib.gacq_ca_code.argtypes = [C.c_int32, C.c_void_p]
+    if lib.gacq_version() != 1:
+        raise ImportError("libgacq ABI version mismatch")
+    return lib
+
+
+_LIB = None
+
+
+def __getattr__(name):
+    """`_lib.lib` loads libgacq.so on first use (so the in-tree build can run before it)."""
+    global _LIB
+    if name == "lib":
+        if _LIB is None:
+            _LIB = _load()
+        return _LIB
+    raise AttributeError(name)
+
+
+def check(rc: int) -> None:
+    if rc == OK:
+        return
+    msg = (__getattr__("lib").gacq_last_error() or b"").decode()
+    if rc == ERR_INVALID:
+        raise InvalidInputError(msg)
+    if rc == ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    raise ResourceError(msg or f"libgacq error {rc}")

@@ -1,0 +1,549 @@
+// gacq.cu -- libgacq.so: C ABI (include/gacq.h) + plan/table construction + launch pipeline.
+//
+// Host-side responsibilities (the kernels are in gacq_kernels.cuh):
+//   * validation mirroring acquisition.py:114-126 (lengths) and 201-204 (PRN list),
+//   * bit-exact NCO tables: carrier replicas (kernels.py:61-62,106-114) and the
+//     code chip-index sequence (kernels.py:65-70,116-128) used to prove the
+//     chip-aligned structure the device algorithm relies on,
+//   * conjugate code spectra (acquisition.py:84-105) computed in float64,
+//   * a chunked K1 -> K2 launch pipeline over (snapshot, bin) pairs with the H2D of
+//     the next snapshots overlapped on a copy stream, then K3 and one D2H.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "gacq_kernels.cuh"
+
+using namespace gacq;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(GACQ_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));       \
+    } while (0)
+
+constexpr int64_t kCarrierScale = int64_t(1) << 48;
+constexpr int64_t kCodeScale = int64_t(1) << 42;
+constexpr int64_t kCodeModulus = int64_t(1023) << 42;
+constexpr double kChipRate = 1.023e6;
+constexpr double kTwoPi = 2.0 * 3.14159265358979323846;
+
+// Python's int(round(x)) on a finite double: round-half-even (nearbyint, default mode)
+int64_t py_round(double x) { return (int64_t)std::nearbyint(x); }
+
+int64_t py_mod(int64_t a, int64_t m) {
+    int64_t r = a % m;
+    return r < 0 ? r + m : r;
+}
+
+// cacode.py:41-58 -- G1 taps 3,10; G2 taps 2,3,6,8,9,10; output G1[10]^G2[s1]^G2[s2]
+const int kG2Select[32][2] = {{2, 6},  {3, 7},  {4, 8},  {5, 9},  {1, 9},  {2, 10}, {1, 8},  {2, 9},
+                              {3, 10}, {2, 3},  {3, 4},  {5, 6},  {6, 7},  {7, 8},  {8, 9},  {9, 10},
+                              {1, 4},  {2, 5},  {3, 6},  {4, 7},  {5, 8},  {6, 9},  {1, 3},  {4, 6},
+                              {5, 7},  {6, 8},  {7, 9},  {8, 10}, {1, 6},  {2, 7},  {3, 8},  {4, 9}};
+
+void ca_code(int prn, int8_t* out) {
+    int g1[10], g2[10];
+    for (int i = 0; i < 10; ++i) g1[i] = g2[i] = 1;
+    const int s1 = kG2Select[prn - 1][0] - 1, s2 = kG2Select[prn - 1][1] - 1;
+    for (int i = 0; i < 1023; ++i) {
+        out[i] = (g1[9] ^ g2[s1] ^ g2[s2]) ? 1 : -1;
+        const int f1 = g1[2] ^ g1[9];
+        const int f2 = g2[1] ^ g2[2] ^ g2[5] ^ g2[7] ^ g2[8] ^ g2[9];
+        for (int k = 9; k > 0; --k) { g1[k] = g1[k - 1]; g2[k] = g2[k - 1]; }
+        g1[0] = f1;
+        g2[0] = f2;
+    }
+}
+
+// iterative radix-2 complex FFT in float64, sign -1 (forward)
+void fft_f64(std::vector<std::complex<double>>& a) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    for (size_t len = 2; len <= n; len <<= 1) {
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < len / 2; ++k) {
+                const double ang = -kTwoPi * (double)k / (double)len;
+                const std::complex<double> w(std::cos(ang), std::sin(ang));
+                const auto u = a[i + k], v = a[i + k + len / 2] * w;
+                a[i + k] = u + v;
+                a[i + k + len / 2] = u - v;
+            }
+    }
+}
+
+// natural index n of a 2048-point spectrum -> float2 slot of the permuted layout that
+// lets thread t of a 128-thread transform fetch x[t + 128 r'] as 8 float4 loads
+inline int perm_slot(int n) {
+    const int rp = n >> 7, t = n & 127;
+    return (rp >> 1) * 256 + 2 * t + (rp & 1);
+}
+
+}  // namespace
+
+struct gacq_ctx {
+    std::mutex mu;
+    int device = 0;
+    double fs = 0;
+    int n_coh = 0, P = 0, D = 0, K = 0, R = 0, B = 0, n_prn = 0, radius = 0;
+    int ng = 1;  // K1 transform groups per CTA
+    std::vector<double> bins;
+    std::vector<int32_t> prns;
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    float2* d_carrier = nullptr;
+    float4* d_cc = nullptr;
+    float2* d_tw = nullptr;
+    float4* d_Z = nullptr;
+    int64_t z_pairs = 0;  // pairs per chunk that fit in the scratch
+    float2* d_in = nullptr;
+    int64_t in_cap = 0;   // snapshots
+    gacq_row* d_rows_bin = nullptr;
+    int64_t rows_bin_cap = 0;
+    gacq_row* d_rows = nullptr;
+    int64_t rows_cap = 0;
+    float* d_pmap = nullptr;
+    float* d_row_scratch = nullptr;  // [z_pairs*n_prn][D*1024] power rows when D > 4
+    std::vector<cudaEvent_t> copy_events;
+    std::vector<cudaEvent_t> prof_events;
+    gacq_stats stats{};
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+int grow(T** ptr, int64_t* cap, int64_t need) {
+    if (need <= *cap) return GACQ_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    if (cudaMalloc((void**)ptr, sizeof(T) * (size_t)need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GACQ_ERR_RESOURCE, "cudaMalloc of %lld bytes failed", (long long)(sizeof(T) * need));
+    }
+    *cap = need;
+    return GACQ_OK;
+}
+
+int fwd_row_stride(const gacq_ctx* c) { return kRow + (c->D <= 16 ? 16 / c->D : 0); }
+int fwd_smem_bytes(const gacq_ctx* c) {
+    return (int)sizeof(float2) * (c->D * fwd_row_stride(c) + c->ng * 2 * kXchg);
+}
+bool corr_row_in_smem(const gacq_ctx* c) { return c->D <= 4; }
+int corr_smem_bytes(const gacq_ctx* c) { return corr_row_in_smem(c) ? (int)sizeof(float) * c->D * kRow : 0; }
+
+cudaError_t launch_fwd(const gacq_ctx* c, const FwdArgs& fa, int64_t blocks) {
+    const int smem = fwd_smem_bytes(c);
+    switch (c->ng) {
+        case 2: gacq_fwd_kernel<2><<<(unsigned)blocks, 2 * kT, smem, c->stream>>>(fa); break;
+        default: gacq_fwd_kernel<1><<<(unsigned)blocks, kT, smem, c->stream>>>(fa); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_corr(const gacq_ctx* c, const CorrArgs& ca, int64_t blocks) {
+    if (corr_row_in_smem(c))
+        gacq_corr_kernel<true><<<(unsigned)blocks, kT, corr_smem_bytes(c), c->stream>>>(ca);
+    else
+        gacq_corr_kernel<false><<<(unsigned)blocks, kT, corr_smem_bytes(c), c->stream>>>(ca);
+    return cudaGetLastError();
+}
+
+cudaEvent_t prof_event(gacq_ctx* c, size_t i) {
+    while (c->prof_events.size() <= i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->prof_events.push_back(e);
+    }
+    return c->prof_events[i];
+}
+
+// Core pipeline. `src` is a device pointer when on_device, else a host pointer.
+int run_impl(gacq_ctx* c, const float2* src, int64_t n_snap, int64_t stride, bool on_device, bool per_bin,
+             bool profile, gacq_row* rows_out, bool rows_on_device, float* pmap) {
+    const int64_t span = (int64_t)c->R * c->n_coh;
+    const int64_t n_pairs = n_snap * c->B;
+    const int64_t n_rows = n_snap * c->n_prn;
+    int rc;
+    if ((rc = grow(&c->d_rows_bin, &c->rows_bin_cap, n_rows * c->B))) return rc;
+    if (!per_bin && (rc = grow(&c->d_rows, &c->rows_cap, n_rows))) return rc;
+
+    cudaEvent_t run_start = nullptr, run_end = nullptr;
+    if (profile) {
+        run_start = prof_event(c, 0);
+        run_end = prof_event(c, 1);
+        CUDA_TRY(cudaEventRecord(run_start, on_device ? c->stream : c->copy_stream));
+    }
+    const float2* in = src;
+    int64_t in_stride = stride;
+    // H2D in snapshot chunks on the copy stream; chunk k is covered by copy_events[k]
+    int64_t copy_chunk = 0, n_copy_chunks = 0;
+    if (!on_device) {
+        if ((rc = grow(&c->d_in, &c->in_cap, n_snap * span))) return rc;
+        in = c->d_in;
+        in_stride = span;
+        copy_chunk = std::max<int64_t>(1, std::min<int64_t>(n_snap, c->z_pairs / c->B));
+        n_copy_chunks = (n_snap + copy_chunk - 1) / copy_chunk;
+        while ((int64_t)c->copy_events.size() < n_copy_chunks) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->copy_events.push_back(e);
+        }
+        for (int64_t k = 0; k < n_copy_chunks; ++k) {
+            const int64_t s0 = k * copy_chunk, ns = std::min(copy_chunk, n_snap - s0);
+            CUDA_TRY(cudaMemcpy2DAsync(c->d_in + s0 * span, span * sizeof(float2), src + s0 * stride,
+                                       stride * sizeof(float2), span * sizeof(float2), ns,
+                                       cudaMemcpyHostToDevice, c->copy_stream));
+            CUDA_TRY(cudaEventRecord(c->copy_events[k], c->copy_stream));
+        }
+        c->stats.h2d_bytes += n_snap * span * (int64_t)sizeof(float2);
+    }
+
+    size_t ev = 2;
+    int64_t waited = -1;
+    std::vector<std::pair<size_t, int>> timed;  // (event index, kernel kind)
+    for (int64_t p0 = 0; p0 < n_pairs; p0 += c->z_pairs) {
+        const int64_t np = std::min(c->z_pairs, n_pairs - p0);
+        if (!on_device) {
+            const int64_t last_snap = (p0 + np - 1) / c->B;
+            const int64_t need = last_snap / copy_chunk;
+            for (int64_t k = waited + 1; k <= need; ++k)
+                CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[k], 0));
+            waited = std::max(waited, need);
+        }
+        FwdArgs fa{in, in_stride, c->d_carrier, c->d_tw, c->d_Z, p0, c->B, c->R, c->n_coh, c->P, c->D, c->K,
+                   fwd_row_stride(c)};
+        if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
+        CUDA_TRY(launch_fwd(c, fa, np * c->R));
+        if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
+        CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, c->B, c->R, c->D, c->P,
+                    c->n_prn, c->radius};
+        if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
+        CUDA_TRY(launch_corr(c, ca, np * c->n_prn));
+        if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
+        c->stats.fwd_launches++;
+        c->stats.corr_launches++;
+        c->stats.launches += 2;
+    }
+    const gacq_row* result = c->d_rows_bin;
+    int64_t n_out = n_rows * c->B;
+    if (!per_bin) {
+        if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 2}); }
+        const int64_t threads = n_rows * 32;
+        gacq_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, c->stream>>>(c->d_rows_bin, c->d_rows,
+                                                                                    n_rows, c->B);
+        CUDA_TRY(cudaGetLastError());
+        if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
+        c->stats.reduce_launches++;
+        c->stats.launches++;
+        result = c->d_rows;
+        n_out = n_rows;
+    }
+    if (rows_out) {
+        if (rows_on_device) {
+            CUDA_TRY(cudaMemcpyAsync(rows_out, result, n_out * sizeof(gacq_row), cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(rows_out, result, n_out * sizeof(gacq_row), cudaMemcpyDeviceToHost, c->stream));
+            c->stats.d2h_bytes += n_out * (int64_t)sizeof(gacq_row);
+        }
+    }
+    if (profile) CUDA_TRY(cudaEventRecord(run_end, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (!on_device) CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
+    if (profile) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, run_start, run_end));
+        c->stats.run_ms += ms;
+    }
+    for (auto& te : timed) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->prof_events[te.first], c->prof_events[te.first + 1]));
+        (te.second == 0 ? c->stats.fwd_ms : te.second == 1 ? c->stats.corr_ms : c->stats.reduce_ms) += ms;
+    }
+    c->stats.calls++;
+    c->stats.cells += n_snap * c->n_prn * c->B;
+    return GACQ_OK;
+}
+
+void destroy_ctx(gacq_ctx* c) {
+    if (!c) return;
+    {
+        DeviceGuard g(c->device);
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        cudaFree(c->d_carrier);
+        cudaFree(c->d_cc);
+        cudaFree(c->d_tw);
+        cudaFree(c->d_Z);
+        cudaFree(c->d_in);
+        cudaFree(c->d_rows_bin);
+        cudaFree(c->d_rows);
+        cudaFree(c->d_pmap);
+        cudaFree(c->d_row_scratch);
+        for (auto e : c->copy_events) cudaEventDestroy(e);
+        for (auto e : c->prof_events) cudaEventDestroy(e);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    }
+    delete c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gacq_version(void) { return GACQ_ABI_VERSION; }
+
+const char* gacq_last_error(void) { return g_last_error.c_str(); }
+
+int gacq_ca_code(int32_t prn, int8_t* out) {
+    if (prn < 1 || prn > 32) return fail(GACQ_ERR_INVALID, "prn must be an integer in 1..32, got %d", prn);
+    if (!out) return fail(GACQ_ERR_INVALID, "null output");
+    ca_code(prn, out);
+    return GACQ_OK;
+}
+
+int gacq_create(gacq_ctx** out, const gacq_params* p) {
+    if (!out || !p) return fail(GACQ_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (!(p->sample_rate_hz > 0) || !std::isfinite(p->sample_rate_hz))
+        return fail(GACQ_ERR_INVALID, "sample_rate_hz must be > 0");
+    if (p->coherent_ms < 1 || p->noncoherent_rounds < 1)
+        return fail(GACQ_ERR_INVALID, "coherent_ms and noncoherent_rounds must be >= 1");
+    if (p->n_bins < 1 || !p->doppler_bins_hz) return fail(GACQ_ERR_INVALID, "need >= 1 Doppler bin");
+    if (p->exclusion_radius_samples < 0) return fail(GACQ_ERR_INVALID, "exclusion_radius_samples must be >= 0");
+    if (p->n_prn < 1 || p->n_prn > 32 || !p->prns) return fail(GACQ_ERR_INVALID, "prns must be non-empty (<= 32)");
+    for (int i = 0; i < p->n_prn; ++i) {
+        if (p->prns[i] < 1 || p->prns[i] > 32)
+            return fail(GACQ_ERR_INVALID, "prn must be an integer in 1..32, got %d", p->prns[i]);
+        for (int j = 0; j < i; ++j)
+            if (p->prns[j] == p->prns[i]) return fail(GACQ_ERR_INVALID, "prns must be distinct");
+    }
+    const double fs = p->sample_rate_hz;
+    const int64_t n_coh = py_round(fs * p->coherent_ms * 1e-3);        // acquisition.py:116
+    const int64_t P = py_round(fs * 1023.0 / kChipRate);              // acquisition.py:108-109
+    if (n_coh < P) return fail(GACQ_ERR_INVALID, "coherent window shorter than one code period");
+    // chip-aligned structure required by the device algorithm
+    if (P % 1023 != 0 || n_coh % P != 0)
+        return fail(GACQ_ERR_UNSUPPORTED,
+                    "fs=%.17g Hz: the GPU path needs fs = D*1.023 MHz (integer D) and n_coh a multiple of the "
+                    "code period (got P=%lld, n_coh=%lld)", fs, (long long)P, (long long)n_coh);
+    const int D = (int)(P / 1023), K = (int)(n_coh / P);
+    if (D > 64) return fail(GACQ_ERR_UNSUPPORTED, "chip oversampling D=%d > 64 not supported", D);
+    {   // the reference's replica must index chips exactly as floor(n/D) mod 1023 (kernels.py:116-128)
+        const int64_t step = py_round((kChipRate / fs) * (double)kCodeScale);
+        int64_t ph = 0;
+        for (int64_t n = 0; n < n_coh; ++n) {
+            if ((ph >> 42) != (n / D) % 1023)
+                return fail(GACQ_ERR_UNSUPPORTED, "code NCO at fs=%.17g Hz is not chip-aligned at sample %lld", fs,
+                            (long long)n);
+            ph = (ph + step) % kCodeModulus;
+        }
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(GACQ_ERR_CUDA, "no CUDA device visible");
+    }
+    if (p->device < 0 || p->device >= ndev) return fail(GACQ_ERR_INVALID, "device %d out of range", p->device);
+
+    gacq_ctx* c = new gacq_ctx();
+    c->device = p->device;
+    c->fs = fs;
+    c->n_coh = (int)n_coh;
+    c->P = (int)P;
+    c->D = D;
+    c->K = K;
+    c->R = p->noncoherent_rounds;
+    c->B = p->n_bins;
+    c->n_prn = p->n_prn;
+    c->radius = p->exclusion_radius_samples ? p->exclusion_radius_samples : (int)std::ceil(fs / kChipRate);
+    c->ng = D >= 2 ? 2 : 1;
+    c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
+    c->prns.assign(p->prns, p->prns + p->n_prn);
+
+    // ---- host tables --------------------------------------------------------------
+    // carrier replicas, bit-identical to kernels.py:106-114 (phase 0, acquisition.py:139)
+    std::vector<float2> carrier((size_t)c->B * n_coh);
+    {
+        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 16));
+        std::vector<std::thread> th;
+        for (int w = 0; w < nt; ++w)
+            th.emplace_back([&, w]() {
+                for (int b = w; b < c->B; b += nt) {
+                    const int64_t step = py_mod(py_round((c->bins[b] / fs) * (double)kCarrierScale), kCarrierScale);
+                    const double inv = kTwoPi / (double)kCarrierScale;
+                    float2* o = carrier.data() + (size_t)b * n_coh;
+                    for (int64_t k = 0; k < n_coh; ++k) {
+                        const uint64_t ph = ((uint64_t)k * (uint64_t)step) & (uint64_t)(kCarrierScale - 1);
+                        const double th = (double)ph * inv;
+                        o[k] = make_float2((float)std::cos(th), (float)(-std::sin(th)));
+                    }
+                }
+            });
+        for (auto& t : th) t.join();
+    }
+    // conjugate code spectra / 2048 of d[j] = chip[j mod 1023], j < 2046
+    std::vector<float2> cc((size_t)c->n_prn * kM);
+    for (int i = 0; i < c->n_prn; ++i) {
+        int8_t chips[1023];
+        ca_code(c->prns[i], chips);
+        std::vector<std::complex<double>> d(kM, 0.0);
+        for (int j = 0; j < 2 * 1023; ++j) d[j] = (double)chips[j % 1023];
+        fft_f64(d);
+        for (int k = 0; k < kM; ++k) {
+            const auto v = std::conj(d[k]) / (double)kM;
+            cc[(size_t)i * kM + perm_slot(k)] = make_float2((float)v.real(), (float)v.imag());
+        }
+    }
+    std::vector<float2> tw(kM);
+    for (int e = 0; e < kM; ++e) tw[e] = make_float2((float)std::cos(kTwoPi * e / kM), (float)std::sin(kTwoPi * e / kM));
+
+    // ---- device state ---------------------------------------------------------------
+    DeviceGuard guard(c->device);
+    auto bail = [&](int code) {
+        destroy_ctx(c);
+        return code;
+    };
+#define CTX_TRY(expr)                                                                                  \
+    do {                                                                                               \
+        cudaError_t _e = (expr);                                                                       \
+        if (_e != cudaSuccess) return bail(fail(GACQ_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e))); \
+    } while (0)
+    CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CTX_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    CTX_TRY(cudaMalloc(&c->d_carrier, carrier.size() * sizeof(float2)));
+    CTX_TRY(cudaMalloc(&c->d_cc, cc.size() * sizeof(float2)));
+    CTX_TRY(cudaMalloc(&c->d_tw, tw.size() * sizeof(float2)));
+    CTX_TRY(cudaMemcpy(c->d_carrier, carrier.data(), carrier.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    CTX_TRY(cudaMemcpy(c->d_cc, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    CTX_TRY(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    const int64_t pair_bytes = (int64_t)c->R * c->D * kM * (int64_t)sizeof(float2);
+    const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
+    c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
+    CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
+    const int fsm = fwd_smem_bytes(c), csm = corr_smem_bytes(c);
+    if (!corr_row_in_smem(c))
+        CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->z_pairs * c->n_prn * c->D * kRow * sizeof(float)));
+    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
+    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+#undef CTX_TRY
+    *out = c;
+    return GACQ_OK;
+}
+
+int gacq_info_get(const gacq_ctx* c, gacq_info* o) {
+    if (!c || !o) return fail(GACQ_ERR_INVALID, "null argument");
+    o->samples_per_period = c->P;
+    o->n_coh = c->n_coh;
+    o->chip_oversample = c->D;
+    o->fft_len = kM;
+    o->n_bins = c->B;
+    o->n_prn = c->n_prn;
+    o->rounds = c->R;
+    o->path = 1;
+    return GACQ_OK;
+}
+
+void gacq_destroy(gacq_ctx* c) { destroy_ctx(c); }
+
+int gacq_run(gacq_ctx* c, const void* snaps, int64_t n_snap, int64_t stride, uint32_t flags, gacq_row* rows) {
+    if (!c) return fail(GACQ_ERR_INVALID, "null context");
+    if (n_snap < 1) return fail(GACQ_ERR_INVALID, "n_snap must be >= 1");
+    if (!snaps || !rows) return fail(GACQ_ERR_INVALID, "null buffer");
+    const int64_t span = (int64_t)c->R * c->n_coh;
+    if (stride < span && n_snap > 1)
+        return fail(GACQ_ERR_INVALID, "stride %lld < %lld samples needed per snapshot", (long long)stride,
+                    (long long)span);
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return run_impl(c, (const float2*)snaps, n_snap, std::max(stride, span), flags & GACQ_SNAPS_ON_DEVICE,
+                    flags & GACQ_ROWS_PER_BIN, flags & GACQ_PROFILE, rows, flags & GACQ_ROWS_ON_DEVICE, nullptr);
+}
+
+int gacq_power_map(gacq_ctx* c, const void* snap, float* out) {
+    if (!c || !snap || !out) return fail(GACQ_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    const size_t n = (size_t)c->n_prn * c->B * c->P;
+    if (!c->d_pmap && cudaMalloc(&c->d_pmap, n * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GACQ_ERR_RESOURCE, "cudaMalloc power map failed");
+    }
+    const int64_t span = (int64_t)c->R * c->n_coh;
+    int rc = run_impl(c, (const float2*)snap, 1, span, false, true, false, nullptr, false, c->d_pmap);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy(out, c->d_pmap, n * sizeof(float), cudaMemcpyDeviceToHost));
+    return GACQ_OK;
+}
+
+int gacq_host_alloc(int64_t bytes, void** out) {
+    if (!out || bytes <= 0) return fail(GACQ_ERR_INVALID, "bad host allocation request");
+    if (cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(GACQ_ERR_RESOURCE, "cudaHostAlloc of %lld bytes failed", (long long)bytes);
+    }
+    return GACQ_OK;
+}
+
+int gacq_host_free(void* ptr) {
+    if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+    return GACQ_OK;
+}
+
+int gacq_stats_get(const gacq_ctx* c, gacq_stats* o) {
+    if (!c || !o) return fail(GACQ_ERR_INVALID, "null argument");
+    *o = c->stats;
+    return GACQ_OK;
+}
+
+int gacq_stats_reset(gacq_ctx* c) {
+    if (!c) return fail(GACQ_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->stats = gacq_stats{};
+    return GACQ_OK;
+}
+
+}  // extern "C"
