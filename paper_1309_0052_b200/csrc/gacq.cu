@@ -131,7 +131,9 @@ struct gacq_ctx {
     gacq_row* d_rows = nullptr;
     int64_t rows_cap = 0;
     float* d_pmap = nullptr;
-    float* d_row_scratch = nullptr;  // [z_pairs*n_prn][D*1024] power rows when D > 4
+    float* d_row_scratch = nullptr;  // [corr_slots][D*1024] power rows when D > 4
+    int64_t corr_slots = 0;          // resident K2 CTAs (persistent grid)
+    unsigned long long* d_counter = nullptr;  // K2 work counter
     std::vector<cudaEvent_t> copy_events;
     std::vector<cudaEvent_t> prof_events;
     gacq_stats stats{};
@@ -164,23 +166,35 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
     return GACQ_OK;
 }
 
-int fwd_row_stride(const gacq_ctx* c) { return kRow + (c->D <= 16 ? 16 / c->D : 0); }
-int fwd_smem_bytes(const gacq_ctx* c) {
-    return (int)sizeof(float2) * (c->D * fwd_row_stride(c) + c->ng * 2 * kXchg);
-}
+int fwd_smem_bytes(const gacq_ctx* c) { return (int)sizeof(float2) * (c->D * fwd_ws(c->D) + c->ng * 2 * kXchg); }
 bool corr_row_in_smem(const gacq_ctx* c) { return c->D <= 4; }
 int corr_smem_bytes(const gacq_ctx* c) { return corr_row_in_smem(c) ? (int)sizeof(float) * c->D * kRow : 0; }
 
+// K1 instantiations: (transform groups per CTA, chip oversampling D) for every D <= 16 at
+// which the reference's 42-bit code NCO is exactly chip-aligned (checked in gacq_create)
+#define GACQ_FWD_VARIANTS(X) X(1, 1) X(2, 2) X(2, 4) X(2, 5) X(2, 6) X(2, 8) X(2, 13) X(2, 14) X(2, 16)
+
 cudaError_t launch_fwd(const gacq_ctx* c, const FwdArgs& fa, int64_t blocks) {
     const int smem = fwd_smem_bytes(c);
-    switch (c->ng) {
-        case 2: gacq_fwd_kernel<2><<<(unsigned)blocks, 2 * kT, smem, c->stream>>>(fa); break;
-        default: gacq_fwd_kernel<1><<<(unsigned)blocks, kT, smem, c->stream>>>(fa); break;
+#define GACQ_LAUNCH_FWD(NG, DD)                                                       \
+    if (c->D == DD) {                                                                 \
+        gacq_fwd_kernel<NG, DD><<<(unsigned)blocks, NG * kT, smem, c->stream>>>(fa); \
+        return cudaGetLastError();                                                    \
     }
-    return cudaGetLastError();
+    GACQ_FWD_VARIANTS(GACQ_LAUNCH_FWD)
+#undef GACQ_LAUNCH_FWD
+    return cudaErrorInvalidConfiguration;
 }
 
-cudaError_t launch_corr(const gacq_ctx* c, const CorrArgs& ca, int64_t blocks) {
+bool fwd_supported(int D) {
+#define GACQ_HAS_FWD(NG, DD) if (D == DD) return true;
+    GACQ_FWD_VARIANTS(GACQ_HAS_FWD)
+#undef GACQ_HAS_FWD
+    return false;
+}
+
+cudaError_t launch_corr(const gacq_ctx* c, const CorrArgs& ca) {
+    const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
     if (corr_row_in_smem(c))
         gacq_corr_kernel<true><<<(unsigned)blocks, kT, corr_smem_bytes(c), c->stream>>>(ca);
     else
@@ -250,15 +264,15 @@ int run_impl(gacq_ctx* c, const float2* src, int64_t n_snap, int64_t stride, boo
                 CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[k], 0));
             waited = std::max(waited, need);
         }
-        FwdArgs fa{in, in_stride, c->d_carrier, c->d_tw, c->d_Z, p0, c->B, c->R, c->n_coh, c->P, c->D, c->K,
-                   fwd_row_stride(c)};
+        FwdArgs fa{in, in_stride, c->d_carrier, c->d_tw, c->d_Z, p0, c->B, c->R, c->n_coh, c->P, c->D, c->K};
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
         CUDA_TRY(launch_fwd(c, fa, np * c->R));
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
-        CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, c->B, c->R, c->D, c->P,
-                    c->n_prn, c->radius};
+        CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
+        CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, np * c->n_prn,
+                    c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius};
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
-        CUDA_TRY(launch_corr(c, ca, np * c->n_prn));
+        CUDA_TRY(launch_corr(c, ca));
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
         c->stats.fwd_launches++;
         c->stats.corr_launches++;
@@ -318,6 +332,7 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_rows);
         cudaFree(c->d_pmap);
         cudaFree(c->d_row_scratch);
+        cudaFree(c->d_counter);
         for (auto e : c->copy_events) cudaEventDestroy(e);
         for (auto e : c->prof_events) cudaEventDestroy(e);
         if (c->stream) cudaStreamDestroy(c->stream);
@@ -367,7 +382,8 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
                     "fs=%.17g Hz: the GPU path needs fs = D*1.023 MHz (integer D) and n_coh a multiple of the "
                     "code period (got P=%lld, n_coh=%lld)", fs, (long long)P, (long long)n_coh);
     const int D = (int)(P / 1023), K = (int)(n_coh / P);
-    if (D > 64) return fail(GACQ_ERR_UNSUPPORTED, "chip oversampling D=%d > 64 not supported", D);
+    if (!fwd_supported(D))
+        return fail(GACQ_ERR_UNSUPPORTED, "chip oversampling D=%d (fs=%.17g Hz) has no device variant", D, fs);
     {   // the reference's replica must index chips exactly as floor(n/D) mod 1023 (kernels.py:116-128)
         const int64_t step = py_round((kChipRate / fs) * (double)kCodeScale);
         int64_t ph = 0;
@@ -461,13 +477,26 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
     const int fsm = fwd_smem_bytes(c), csm = corr_smem_bytes(c);
-    if (!corr_row_in_smem(c))
-        CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->z_pairs * c->n_prn * c->D * kRow * sizeof(float)));
-    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
-    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
     CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
     CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    {
+        int per_sm = 0, sms = 0;
+        if (corr_row_in_smem(c))
+            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_kernel<true>, kT, csm));
+        else
+            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_kernel<false>, kT, 0));
+        CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+        c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
+    }
+    if (!corr_row_in_smem(c))
+        CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kRow * sizeof(float)));
+    CTX_TRY(cudaMalloc(&c->d_counter, sizeof(unsigned long long)));
+#define GACQ_ATTR_FWD(NG, DM) \
+    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<NG, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+    GACQ_FWD_VARIANTS(GACQ_ATTR_FWD)
+#undef GACQ_ATTR_FWD
+
 #undef CTX_TRY
     *out = c;
     return GACQ_OK;

@@ -33,6 +33,9 @@ constexpr int kT = 128;         // threads per transform (16 points each)
 constexpr int kChips = 1023;
 constexpr int kRow = 1024;      // phase-major power row stride (floats)
 constexpr int kXchg = 2176;     // padded exchange buffer (float2): pad(2047)+1, pad(i) = i + i/16
+#ifndef GACQ_CORR_MIN_BLOCKS
+#define GACQ_CORR_MIN_BLOCKS 3
+#endif
 
 __device__ __forceinline__ void group_sync(int id) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kT) : "memory");
@@ -133,15 +136,19 @@ struct FwdArgs {
     float4* Z;             // [pairs][R][D][1024] float4 spectra (permuted layout)
     int64_t pair0;         // first (snapshot, bin) pair of this chunk, pair = s*B + b
     int B, R, n_coh, P, D, K;
-    int ws;                // row stride of the transposed wiped block (float2), 1024 + 16/D
 };
 
+// Row stride of the transposed wiped block wt[k][m] = wbar[D m + k]: the +16/D pad makes
+// both the wipe stores (consecutive n) and the chip-sum loads (consecutive m) conflict-free.
+__host__ __device__ constexpr int fwd_ws(int D) { return kRow + (D <= 16 ? 16 / D : 0); }
+
 // grid: (pairs_in_chunk * R) blocks of NG*128 threads;
-// dynamic smem: D*ws + NG*2*kXchg float2
-template <int NG>
+// dynamic smem: (D*fwd_ws(D) + NG*2*kXchg) cx
+template <int NG, int D>
 __global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
+    constexpr int WS = fwd_ws(D);
     extern __shared__ cx smem[];
-    cx* wt = smem;  // wt[k*ws + m] = wbar[D*m + k]  (conflict-free chip-sum reads)
+    cx* wt = smem;
     const int lp = blockIdx.x / a.R, rd = blockIdx.x % a.R;
     const int64_t pair = a.pair0 + lp;
     const int64_t s = pair / a.B;
@@ -149,18 +156,21 @@ __global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
     const cx* x = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh;
     const cx* c = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
 
-    // wipe-off (bit-exact, acquisition.py:141) folded over the K code periods
+    // (A) wipe-off (bit-exact, acquisition.py:141) folded over the K code periods, coalesced
+    //     two samples per 16-byte load; wt[k][1023] repeats wt[k][0] (circular chip m+1).
     constexpr int NT = NG * kT;
+    auto put = [&](int n, cx w) {
+        const int m = n / D, k = n - m * D;
+        wt[k * WS + m] = w;
+        if (m == 0) wt[k * WS + kChips] = w;
+    };
     const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0 && (a.P & 1) == 0;
     if (vec) {
-        // two samples per 16-byte load, four loads of each operand in flight per thread
         const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x);
         const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(c);
         const int np = a.P / 2;
         for (int base = threadIdx.x; base < np; base += 4 * NT) {
             cx w[4][2];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) w[u][0] = w[u][1] = czero();
             for (int k = 0; k < a.K; ++k) {
                 ulonglong2 xv[4], cv[4];
 #pragma unroll
@@ -182,11 +192,8 @@ __global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
             for (int u = 0; u < 4; ++u) {
                 const int i = base + u * NT;
                 if (i < np) {
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int n = 2 * i + e, m = n / a.D;
-                        wt[(n - m * a.D) * a.ws + m] = w[u][e];
-                    }
+                    put(2 * i, w[u][0]);
+                    put(2 * i + 1, w[u][1]);
                 }
             }
         }
@@ -194,37 +201,50 @@ __global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
         for (int n = threadIdx.x; n < a.P; n += NT) {
             cx acc = cmul_exact(__ldg(&x[n]), __ldg(&c[n]));
             for (int k = 1; k < a.K; ++k) acc = add2(acc, cmul_exact(__ldg(&x[k * a.P + n]), __ldg(&c[k * a.P + n])));
-            const int m = n / a.D;
-            wt[(n - m * a.D) * a.ws + m] = acc;
+            put(n, acc);
         }
     }
     __syncthreads();
 
+    // (B) group g transforms phases g, g+NG, ...; thread t owns chips m = t + 128 r (r < 8),
+    //     exactly its pass-0 inputs: z_rho[m] = sum_{i<D} wbar[D m + rho + i], computed
+    //     directly for the group's first phase and then slid by NG samples per phase.
     const int g = threadIdx.x / kT, t = threadIdx.x % kT;
-    cx* xs0 = smem + a.D * a.ws + g * 2 * kXchg;
+    cx* xs0 = smem + D * WS + g * 2 * kXchg;
     cx* xs1 = xs0 + kXchg;
     cx tw1[16], tw2[8];
     load_twiddles<-1>(a.tw, t, tw1, tw2);
     const XAddr xa = xaddr(t);
     auto sync = [g]() { group_sync(1 + g); };
-    for (int rho = g; rho < a.D; rho += NG) {
-        cx v[16], u[2][8];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = czero();
+    cx z[8];
+    for (int rho = g; rho < D; rho += NG) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const int m = t + 128 * r;
-            if (m < kChips) {
-                // z_rho[m] = sum of the D wiped samples starting at D*m + rho (mod P)
-                cx z = czero();
-                const int m1 = (m + 1 == kChips) ? 0 : m + 1;
-                for (int k = rho; k < a.D; ++k) z = add2(z, wt[k * a.ws + m]);
-                for (int k = 0; k < rho; ++k) z = add2(z, wt[k * a.ws + m1]);
-                v[r] = z;
+            if (m >= kChips) continue;
+            if (D <= 4 || rho == g) {
+                cx acc = czero();
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+                    const int k = rho + i;
+                    acc = add2(acc, k < D ? wt[k * WS + m] : wt[(k - D) * WS + m + 1]);
+                }
+                z[r] = acc;
+            } else {
+#pragma unroll
+                for (int j = 0; j < NG; ++j) {  // window moves from rho-NG to rho
+                    const int k = rho - NG + j;
+                    z[r] = add2(sub2(z[r], wt[k * WS + m]), wt[k * WS + m + 1]);
+                }
             }
         }
+        cx v[16], u[2][8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = (t + 128 * r < kChips) ? z[r] : czero();
+#pragma unroll
+        for (int r = 8; r < 16; ++r) v[r] = czero();
         fft2048<-1>(v, u, xs0, xs1, tw1, tw2, xa, sync);
-        ulonglong2* dst = reinterpret_cast<ulonglong2*>(a.Z) + (((int64_t)lp * a.R + rd) * a.D + rho) * (kM / 2);
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(a.Z) + (((int64_t)lp * a.R + rd) * D + rho) * (kM / 2);
 #pragma unroll
         for (int r = 0; r < 8; ++r) dst[r * 128 + t] = make_ulonglong2(u[0][r], u[1][r]);
     }
@@ -236,145 +256,168 @@ struct CorrArgs {
     const float2* tw;
     gacq_row* rows_bin;    // [n_snap][n_prn][B]
     float* pmap;           // optional [n_prn][B][P] power map (single snapshot), else null
-    float* row_scratch;    // [blocks][D*1024] when the row does not live in shared memory
+    float* row_scratch;    // [gridDim][D*1024] when the row does not live in shared memory
     int64_t pair0;
+    int64_t n_items;       // pairs_in_chunk * n_prn, item = lp * n_prn + pi
+    unsigned long long* counter;  // zeroed before the launch; items >= gridDim.x are claimed here
     int B, R, D, P, n_prn, radius;
 };
 
-// grid: pairs_in_chunk * n_prn blocks of 128 threads; dynamic smem: D*1024 floats if kRowSmem
+// Persistent: gridDim.x = resident CTA slots; CTA c starts with item c and then claims items
+// in order from a global counter, so the in-flight items stay a contiguous window of the
+// pair-major item list and the n_prn CTAs sharing a pair's spectra hit them in L2.
+// 128 threads per CTA; dynamic smem: D*1024 floats if kRowSmem.
 template <bool kRowSmem>
-__global__ void __launch_bounds__(kT, 3) gacq_corr_kernel(CorrArgs a) {
+__global__ void __launch_bounds__(kT, GACQ_CORR_MIN_BLOCKS) gacq_corr_kernel(CorrArgs a) {
     __shared__ cx xs[2][kXchg];
     __shared__ float red_v[kT / 32];
     __shared__ int red_i[kT / 32];
+    __shared__ long long s_next;
     extern __shared__ float row_smem[];  // power row [D][1024] when kRowSmem
     const int t = threadIdx.x;
-    const int lp = blockIdx.x / a.n_prn, pi = blockIdx.x % a.n_prn;
-    const int64_t pair = a.pair0 + lp;
-    const int64_t s = pair / a.B;
-    const int b = (int)(pair % a.B);
     float* row = kRowSmem ? row_smem : a.row_scratch + (int64_t)blockIdx.x * a.D * kRow;
-
-    cx cc[16];
-    const ulonglong2* ccp = reinterpret_cast<const ulonglong2*>(a.Cc) + (int64_t)pi * (kM / 2);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const ulonglong2 q = __ldg(&ccp[i * 128 + t]);
-        cc[2 * i] = q.x;
-        cc[2 * i + 1] = q.y;
-    }
     cx tw1[16], tw2[8];
     load_twiddles<1>(a.tw, t, tw1, tw2);
     const XAddr xa = xaddr(t);
     auto sync = []() { __syncthreads(); };
+    const ulonglong2* Z = reinterpret_cast<const ulonglong2*>(a.Z);
+    const ulonglong2* Cc = reinterpret_cast<const ulonglong2*>(a.Cc);
+    const int64_t pair_span = (int64_t)a.R * a.D * (kM / 2);  // ulonglong2 per pair
+    const int64_t zstep = (int64_t)a.D * (kM / 2);            // next round, same phase
 
-    // work items (rho, rd) in rho-major order; spectra at Z[((lp*R + rd)*D + rho)*1024].
-    // The next item's spectrum is loaded into registers right after the current one has
-    // been consumed by the code product, so its L2 latency hides behind a whole transform.
-    const ulonglong2* zbase = reinterpret_cast<const ulonglong2*>(a.Z) + (int64_t)lp * a.R * a.D * (kM / 2);
-    const int64_t zstep = (int64_t)a.D * (kM / 2);  // next round, same phase
-    ulonglong2 zq[8];
+    int64_t item = blockIdx.x;
+    if (item >= a.n_items) return;
+    // operands of the first transform
+    ulonglong2 zq[8], cq[8];
+    {
+        const ulonglong2* zp = Z + (item / a.n_prn) * pair_span;
+        const ulonglong2* cp = Cc + (item % a.n_prn) * (kM / 2);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) zq[i] = __ldg(zbase + i * 128 + t);
-    float best = -1.f;       // this thread's first argmax over the cells it owns
-    int bidx = 0x7fffffff;
-    for (int rho = 0; rho < a.D; ++rho) {
-        cx acc2[2][4];  // (sum re^2, sum im^2) per owned cell
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) acc2[h][r] = czero();
-        const ulonglong2* zp = zbase + rho * (kM / 2);
-        for (int rd = 0; rd < a.R; ++rd) {
-            cx v[16], u[2][8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                v[2 * i] = cmul(zq[i].x, cc[2 * i]);
-                v[2 * i + 1] = cmul(zq[i].y, cc[2 * i + 1]);
-            }
-            // next item: next round of this phase, else round 0 of the next phase
-            const ulonglong2* zn = (rd + 1 < a.R) ? zp + zstep : zbase + (rho + 1) * (kM / 2);
-            if (rd + 1 < a.R || rho + 1 < a.D) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) zq[i] = __ldg(zn + i * 128 + t);
-            }
-            zp = zn;
-            fft2048<1>(v, u, xs[0], xs[1], tw1, tw2, xa, sync);
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int r = 0; r < 4; ++r) acc2[h][r] = fma2(u[h][4 + r], u[h][4 + r], acc2[h][r]);
+        for (int i = 0; i < 8; ++i) {
+            zq[i] = __ldg(zp + i * 128 + t);
+            cq[i] = __ldg(cp + i * 128 + t);
         }
-        // output k = t + 128 h + 256 (4 + r) -> chip lag q = k - 1025; row[rho*1024 + q]
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int q = t + 128 * h + 256 * (4 + r) - 1025;
-                if (q >= 0) {
-                    const float p = re(acc2[h][r]) + im(acc2[h][r]);
-                    row[rho * kRow + q] = p;
-                    const int lag = a.D * q + rho;
-                    if (p > best || (p == best && lag < bidx)) { best = p; bidx = lag; }
-                }
-            }
     }
-    __syncthreads();
+    for (int64_t next; item < a.n_items; item = next) {
+        if (t == 0) s_next = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
+        __syncthreads();
+        next = s_next;
+        const int64_t lp = item / a.n_prn;
+        const int pi = (int)(item % a.n_prn);
+        const bool has_next = next < a.n_items;
+        const ulonglong2* zbase = Z + lp * pair_span;
+        const ulonglong2* zbase_n = Z + (has_next ? next / a.n_prn : lp) * pair_span;
+        const ulonglong2* cnext = Cc + (has_next ? next % a.n_prn : pi) * (kM / 2);
+        const bool new_prn = has_next && (next % a.n_prn) != pi;
 
-    // first argmax of the row (acquisition.py:151): ties -> lowest lag D*q + rho
+        float best = -1.f;  // this thread's first argmax over the cells it owns
+        int bidx = 0x7fffffff;
+        for (int rho = 0; rho < a.D; ++rho) {
+            cx acc2[2][4];  // (sum re^2, sum im^2) per owned cell
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
-        if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
-    }
-    if ((t & 31) == 0) { red_v[t >> 5] = best; red_i[t >> 5] = bidx; }
-    __syncthreads();
-    best = red_v[0];
-    bidx = red_i[0];
-#pragma unroll
-    for (int w = 1; w < kT / 32; ++w)
-        if (red_v[w] > best || (red_v[w] == best && red_i[w] < bidx)) { best = red_v[w]; bidx = red_i[w]; }
-    const int lag = bidx;
-    // exclusion floor (acquisition.py:155-159): max over lags whose circular distance to
-    // the peak, |((l - lag + P/2) mod P) - P/2| = min(|l - lag|, P - |l - lag|), exceeds radius.
-    // Each thread revisits exactly the cells it wrote.
-    float fl = -1.f;
-    for (int rho = 0; rho < a.D; ++rho)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int q = t + 128 * h + 256 * (4 + r) - 1025;
-                if (q < 0) continue;
-                int d = abs(a.D * q + rho - lag);
-                d = min(d, a.P - d);
-                if (d > a.radius) fl = fmaxf(fl, row[rho * kRow + q]);
-            }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
-    __syncthreads();
-    if ((t & 31) == 0) red_v[t >> 5] = fl;
-    __syncthreads();
-    if (t == 0) {
-        float f = red_v[0];
-#pragma unroll
-        for (int w = 1; w < kT / 32; ++w) f = fmaxf(f, red_v[w]);
-        gacq_row out;
-        out.bin = b;
-        out.lag = lag;
-        out.peak = best;
-        out.floor = f < 0.f ? 0.f : f;
-        a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
-    }
-    if (a.pmap) {
-        float* dst = a.pmap + ((int64_t)pi * a.B + b) * a.P;
-        for (int rho = 0; rho < a.D; ++rho)
             for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc2[h][r] = czero();
+            const ulonglong2* zp = zbase + rho * (kM / 2);
+            for (int rd = 0; rd < a.R; ++rd) {
+                cx v[16], u[2][8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    v[2 * i] = cmul(zq[i].x, cq[i].x);
+                    v[2 * i + 1] = cmul(zq[i].y, cq[i].y);
+                }
+                // prefetch the next transform's spectrum (next round, next phase or next
+                // item) and, when the next item is another PRN, its code spectrum
+                const bool last = rd + 1 == a.R && rho + 1 == a.D;
+                const ulonglong2* zn = rd + 1 < a.R ? zp + zstep : (rho + 1 < a.D ? zbase + (rho + 1) * (kM / 2) : zbase_n);
+                if (!last || has_next) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) zq[i] = __ldg(zn + i * 128 + t);
+                }
+                if (last && new_prn) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) cq[i] = __ldg(cnext + i * 128 + t);
+                }
+                zp = zn;
+                fft2048<1>(v, u, xs[0], xs[1], tw1, tw2, xa, sync);
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc2[h][r] = fma2(u[h][4 + r], u[h][4 + r], acc2[h][r]);
+            }
+            // output k = t + 128 h + 256 (4 + r) -> chip lag q = k - 1025; row[rho*1024 + q]
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const int q = t + 128 * h + 256 * (4 + r) - 1025;
-                    if (q >= 0) dst[a.D * q + rho] = row[rho * kRow + q];
+                    if (q >= 0) {
+                        const float p = re(acc2[h][r]) + im(acc2[h][r]);
+                        row[rho * kRow + q] = p;
+                        const int lag = a.D * q + rho;
+                        if (p > best || (p == best && lag < bidx)) { best = p; bidx = lag; }
+                    }
                 }
+        }
+
+        // first argmax of the row (acquisition.py:151): ties -> lowest lag D*q + rho
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+            if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+        }
+        if ((t & 31) == 0) { red_v[t >> 5] = best; red_i[t >> 5] = bidx; }
+        __syncthreads();
+        best = red_v[0];
+        bidx = red_i[0];
+#pragma unroll
+        for (int w = 1; w < kT / 32; ++w)
+            if (red_v[w] > best || (red_v[w] == best && red_i[w] < bidx)) { best = red_v[w]; bidx = red_i[w]; }
+        const int lag = bidx;
+        // exclusion floor (acquisition.py:155-159): max over lags whose circular distance to
+        // the peak, |((l - lag + P/2) mod P) - P/2| = min(|l - lag|, P - |l - lag|), exceeds
+        // radius. Each thread revisits exactly the cells it wrote.
+        float fl = -1.f;
+        for (int rho = 0; rho < a.D; ++rho)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int q = t + 128 * h + 256 * (4 + r) - 1025;
+                    if (q < 0) continue;
+                    int d = abs(a.D * q + rho - lag);
+                    d = min(d, a.P - d);
+                    if (d > a.radius) fl = fmaxf(fl, row[rho * kRow + q]);
+                }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
+        __syncthreads();
+        if ((t & 31) == 0) red_v[t >> 5] = fl;
+        __syncthreads();
+        const int64_t pair = a.pair0 + lp;
+        const int64_t s = pair / a.B;
+        const int b = (int)(pair % a.B);
+        if (t == 0) {
+            float f = red_v[0];
+#pragma unroll
+            for (int w = 1; w < kT / 32; ++w) f = fmaxf(f, red_v[w]);
+            gacq_row out;
+            out.bin = b;
+            out.lag = lag;
+            out.peak = best;
+            out.floor = f < 0.f ? 0.f : f;
+            a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
+        }
+        if (a.pmap) {
+            float* dst = a.pmap + ((int64_t)pi * a.B + b) * a.P;
+            for (int rho = 0; rho < a.D; ++rho)
+                for (int h = 0; h < 2; ++h)
+                    for (int r = 0; r < 4; ++r) {
+                        const int q = t + 128 * h + 256 * (4 + r) - 1025;
+                        if (q >= 0) dst[a.D * q + rho] = row[rho * kRow + q];
+                    }
+        }
     }
 }
 
