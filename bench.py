@@ -220,8 +220,10 @@ def run_reference(args, rank, world):
     rates, sample = cpu_measure(args.config, cores, args.steps, args.warmup)
     v = statistics.mean(rates)
     c = CONFIGS[args.config]
+    n_bins = len(np.arange(-c["span_hz"], c["span_hz"] + 1e-9, c["step"]))
+    ms = cores * 32 * n_bins / v * 1e3  # one step = one snapshot per process
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32", "data": "synthetic (oracle.make_snapshot)",
             "impl": "reference",
             "config": {"workload": c["desc"], "parallelism": f"{cores} CPU processes"},

@@ -4,11 +4,12 @@ without the built extension raises."""
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import InvalidInputError, ResourceError, UnsupportedError
 
-LIB_PATH = Path(__file__).resolve().parent / "libgacq.so"
+LIB_PATH = Path(os.environ.get("GACQ_LIB") or Path(__file__).resolve().parent / "libgacq.so")
 
 OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_CUDA, ERR_RESOURCE = 0, -1, -2, -3, -4
 SNAPS_ON_DEVICE, ROWS_ON_DEVICE, ROWS_PER_BIN, PROFILE = 1, 2, 4, 8

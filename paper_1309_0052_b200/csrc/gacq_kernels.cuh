@@ -36,6 +36,9 @@ constexpr int kXchg = 2176;     // padded exchange buffer (float2): pad(2047)+1,
 #ifndef GACQ_CORR_MIN_BLOCKS
 #define GACQ_CORR_MIN_BLOCKS 3
 #endif
+#ifndef GACQ_K2_TW1_SMEM
+#define GACQ_K2_TW1_SMEM 0
+#endif
 
 __device__ __forceinline__ void group_sync(int id) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kT) : "memory");
@@ -88,9 +91,10 @@ __device__ __forceinline__ cx w16_mul(cx a, int r) {
     }
 }
 
-template <int S, typename Sync>
+// `tw1(r)` yields the pass-1 twiddle W^(8 (t%16) r) (from registers or a shared table).
+template <int S, typename Tw1, typename Sync>
 __device__ __forceinline__ void fft2048(cx (&v)[16], cx (&u)[2][8], cx* __restrict__ xs0, cx* __restrict__ xs1,
-                                        const cx (&tw1)[16], const cx (&tw2)[8], const XAddr& xa, Sync sync) {
+                                        Tw1 tw1, const cx (&tw2)[8], const XAddr& xa, Sync sync) {
     dft16<S>(v);
 #pragma unroll
     for (int r = 0; r < 16; ++r) xs0[xa.s0 + r] = v[r];
@@ -98,7 +102,7 @@ __device__ __forceinline__ void fft2048(cx (&v)[16], cx (&u)[2][8], cx* __restri
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = xs0[xa.l1 + 136 * r];
 #pragma unroll
-    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], tw1[r]);
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], tw1(r));
     dft16<S>(v);
 #pragma unroll
     for (int r = 0; r < 16; ++r) xs1[xa.s1 + 17 * r] = v[r];
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
         for (int r = 0; r < 8; ++r) v[r] = (t + 128 * r < kChips) ? z[r] : czero();
 #pragma unroll
         for (int r = 8; r < 16; ++r) v[r] = czero();
-        fft2048<-1>(v, u, xs0, xs1, tw1, tw2, xa, sync);
+        fft2048<-1>(v, u, xs0, xs1, [&](int r) { return tw1[r]; }, tw2, xa, sync);
         ulonglong2* dst = reinterpret_cast<ulonglong2*>(a.Z) + (((int64_t)lp * a.R + rd) * D + rho) * (kM / 2);
 #pragma unroll
         for (int r = 0; r < 8; ++r) dst[r * 128 + t] = make_ulonglong2(u[0][r], u[1][r]);
@@ -276,8 +280,30 @@ __global__ void __launch_bounds__(kT, GACQ_CORR_MIN_BLOCKS) gacq_corr_kernel(Cor
     extern __shared__ float row_smem[];  // power row [D][1024] when kRowSmem
     const int t = threadIdx.x;
     float* row = kRowSmem ? row_smem : a.row_scratch + (int64_t)blockIdx.x * a.D * kRow;
-    cx tw1[16], tw2[8];
-    load_twiddles<1>(a.tw, t, tw1, tw2);
+#if GACQ_K2_TW1_SMEM
+    // pass-1 twiddles from a padded [16][17] table: lanes t and t+16 share a row
+    // (broadcast) and the 17-stride keeps the 16 rows on distinct banks
+    __shared__ cx tw1s[16 * 17];
+    for (int i = t; i < 256; i += kT) {
+        const float2 w = __ldg(&a.tw[((i >> 4) * (i & 15) * 8) & (kM - 1)]);
+        tw1s[(i >> 4) * 17 + (i & 15)] = pk(w.x, w.y);
+    }
+    cx tw2[8];
+    {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const float2 w = __ldg(&a.tw[(t * r) & (kM - 1)]);
+            tw2[r] = pk(w.x, w.y);
+        }
+    }
+    const cx* tw1row = tw1s + (t & 15) * 17;
+    auto tw1 = [tw1row](int r) { return tw1row[r]; };
+    __syncthreads();
+#else
+    cx tw1r[16], tw2[8];
+    load_twiddles<1>(a.tw, t, tw1r, tw2);
+    auto tw1 = [&](int r) { return tw1r[r]; };
+#endif
     const XAddr xa = xaddr(t);
     auto sync = []() { __syncthreads(); };
     const ulonglong2* Z = reinterpret_cast<const ulonglong2*>(a.Z);
@@ -313,11 +339,11 @@ __global__ void __launch_bounds__(kT, GACQ_CORR_MIN_BLOCKS) gacq_corr_kernel(Cor
         float best = -1.f;  // this thread's first argmax over the cells it owns
         int bidx = 0x7fffffff;
         for (int rho = 0; rho < a.D; ++rho) {
-            cx acc2[2][4];  // (sum re^2, sum im^2) per owned cell
+            float acc[2][4];  // noncoherent power of the owned cells (acquisition.py:149)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int r = 0; r < 4; ++r) acc2[h][r] = czero();
+                for (int r = 0; r < 4; ++r) acc[h][r] = 0.f;
             const ulonglong2* zp = zbase + rho * (kM / 2);
             for (int rd = 0; rd < a.R; ++rd) {
                 cx v[16], u[2][8];
@@ -343,7 +369,10 @@ __global__ void __launch_bounds__(kT, GACQ_CORR_MIN_BLOCKS) gacq_corr_kernel(Cor
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) acc2[h][r] = fma2(u[h][4 + r], u[h][4 + r], acc2[h][r]);
+                    for (int r = 0; r < 4; ++r) {
+                        const float xr = re(u[h][4 + r]), xi = im(u[h][4 + r]);
+                        acc[h][r] = fmaf(xi, xi, fmaf(xr, xr, acc[h][r]));
+                    }
             }
             // output k = t + 128 h + 256 (4 + r) -> chip lag q = k - 1025; row[rho*1024 + q]
 #pragma unroll
@@ -352,7 +381,7 @@ __global__ void __launch_bounds__(kT, GACQ_CORR_MIN_BLOCKS) gacq_corr_kernel(Cor
                 for (int r = 0; r < 4; ++r) {
                     const int q = t + 128 * h + 256 * (4 + r) - 1025;
                     if (q >= 0) {
-                        const float p = re(acc2[h][r]) + im(acc2[h][r]);
+                        const float p = acc[h][r];
                         row[rho * kRow + q] = p;
                         const int lag = a.D * q + rho;
                         if (p > best || (p == best && lag < bidx)) { best = p; bidx = lag; }

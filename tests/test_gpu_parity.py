@@ -168,3 +168,31 @@ def test_visible_satellites_found(pkg):
                 misses.append((i, prn, round(dop, 1), cph, round(cn0, 1), r["doppler_hz"],
                                r["code_phase_samples"], round(r["peak_metric"], 2)))
     assert total > 10 and hits >= 0.9 * total, (hits, total, misses)
+
+
+@pytest.mark.parametrize("cn0", [30.0, 33.0, 36.0, 39.0, 42.0, 45.0])
+def test_c5_weak_signal_sweep_decisions(pkg, cn0):
+    """BASELINE C5: decisions at C/N0 30-45 dB-Hz vs the CPU oracle on the same inputs
+    (C3 grid, 32 PRNs, 4 snapshots per point): (bin, lag) and `detected` exact except
+    float32-indistinguishable ties (tests/parity.py)."""
+    fs = 4.092e6
+    kw = dict(doppler_min_hz=-5000.0, doppler_max_hz=5000.0, doppler_step_hz=500.0, noncoherent_rounds=10)
+    ocfg = oracle.OracleConfig(**kw)
+    eng = pkg.get_engine(fs, list(range(1, 33)), pkg.AcqConfig(**kw))
+    snaps = [oracle.make_snapshot(i, fs, 10e-3, base_seed=7000 + int(cn0) * 10, cn0_range=(cn0, cn0))[0]
+             for i in range(4)]
+    got = eng.search(np.stack(snaps)).results()
+    ties = exact = 0
+    for x, res in zip(snaps, got):
+        ref = oracle.acquire_all(x, fs, range(1, 33), ocfg)
+        for g, r in zip(res, ref):
+            gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples,
+                      peak_metric=g.peak_metric, detected=g.detected)
+            v = compare(gd, r, ocfg.detection_threshold)
+            if v not in ("exact", "tie"):
+                pm = oracle.acquire_channel(x, fs, r["prn"], ocfg, want_map=True)["power_map"]
+                v = compare(gd, r, ocfg.detection_threshold, pm, ocfg.doppler_bins_hz())
+            assert v in ("exact", "tie"), f"cn0 {cn0} prn {r['prn']}: {v}"
+            exact += v == "exact"
+            ties += v == "tie"
+    assert exact >= 4 * 32 - 1, (exact, ties)
