@@ -115,6 +115,19 @@ void gacq_destroy(gacq_ctx* ctx);
 int gacq_run(gacq_ctx* ctx, const void* snaps, int64_t n_snap, int64_t stride_samples,
              uint32_t flags, gacq_row* rows);
 
+/* Sample formats of gacq_run_quantized: interleaved I/Q integers as in the reference's IF
+ * file payload (iffile.py:3-16, 38-43). */
+#define GACQ_FMT_INT8 0
+#define GACQ_FMT_INT16 1
+
+/* Same search over integer I/Q (the IF-file payload, read_if_file, iffile.py:74-99): each
+ * component becomes float32(float64(q) * (scale / limit)), limit = 127 (int8) or 32767
+ * (int16) -- bit-identical to read_if_file -- on the device, so only 2 or 4 bytes per sample
+ * cross PCIe. `iq` holds n_snap snapshots of 2*stride_samples integers each (host, or device
+ * with GACQ_SNAPS_ON_DEVICE). */
+int gacq_run_quantized(gacq_ctx* ctx, const void* iq, int32_t sample_format, double scale, int64_t n_snap,
+                       int64_t stride_samples, uint32_t flags, gacq_row* rows);
+
 /* Debug/parity hook: the float32 noncoherent power map [n_prn][n_bins][P] of ONE host
  * snapshot (the reference's power_map, acquisition.py:131-149). */
 int gacq_power_map(gacq_ctx* ctx, const void* snap_host, float* out_host);

@@ -23,6 +23,8 @@ from oracle.gnss_oracle import (  # noqa: F401
     code_replica,
     doppler_bins_hz,
     generate_ca_code,
+    if_file_bytes,
+    if_file_decode,
     make_snapshot,
     samples_per_code_period,
     sigma_for_cn0_dbhz,

@@ -311,3 +311,44 @@ def acquire_all(samples: np.ndarray, fs: float, prns, cfg: OracleConfig,
     if len(set(prns)) != len(prns):
         raise ValueError("prns must be distinct")
     return [acquire_channel(samples, fs, p, cfg, want_map) for p in prns]
+
+
+# --- IF sample files (iffile.py:34-99) ---------------------------------------
+
+import struct as _struct  # noqa: E402
+
+_IF_HEADER = _struct.Struct("<8sId2B10sd")  # iffile.py:36
+_IF_FORMATS = {"int8": 0, "int16": 1, "float32": 2}
+_IF_DTYPES = {0: "<i1", 1: "<i2", 2: "<f4"}
+_IF_LIMITS = {0: 127, 1: 32767}
+
+
+def if_file_bytes(samples: np.ndarray, fs: float, sample_format: str) -> bytes:
+    """write_if_file (iffile.py:53-71) to bytes: max-|component| full scale for integers."""
+    fmt = _IF_FORMATS[sample_format]
+    inter = np.empty(2 * samples.shape[0], dtype=np.float64)
+    inter[0::2] = samples.real
+    inter[1::2] = samples.imag
+    if fmt == 2:
+        scale = 1.0
+        payload = inter.astype("<f4").tobytes()
+    else:
+        limit = _IF_LIMITS[fmt]
+        peak = float(np.max(np.abs(inter))) if inter.size else 0.0
+        scale = peak if peak > 0 else 1.0
+        q = np.clip(np.round(inter / scale * limit).astype(np.int64), -limit, limit)
+        payload = q.astype(_IF_DTYPES[fmt]).tobytes()
+    return _IF_HEADER.pack(b"GNSSIF01", 1, fs, fmt, 0, b"\x00" * 10, scale) + payload
+
+
+def if_file_decode(raw: bytes):
+    """read_if_file (iffile.py:74-99): returns (fs, complex64 samples, fmt, scale, raw ints)."""
+    magic, version, fs, fmt, layout, _r, scale = _IF_HEADER.unpack_from(raw)
+    if magic != b"GNSSIF01" or version != 1 or layout != 0 or fmt not in _IF_DTYPES:
+        raise ValueError("bad GNSSIF01 header")
+    ints = np.frombuffer(raw[_IF_HEADER.size:], dtype=_IF_DTYPES[fmt])
+    if fmt == 2:
+        flat = ints.astype(np.float64)
+    else:
+        flat = ints.astype(np.float64) * (scale / _IF_LIMITS[fmt])
+    return fs, (flat[0::2] + 1j * flat[1::2]).astype(np.complex64), fmt, scale, ints

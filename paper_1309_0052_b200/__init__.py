@@ -13,13 +13,16 @@ from .acquisition import (  # noqa: F401
     acquire_all,
     acquire_batch,
     acquire_channel,
+    acquire_if_file,
     default_doppler_step_hz,
     get_engine,
     samples_per_code_period,
 )
 from .buffers import IqBuffer, Precision  # noqa: F401
+from .iffile import IfPayload, read_if_file, read_if_payload, write_if_file  # noqa: F401
 from .cacode import CHIP_RATE_HZ, CODE_LENGTH, CaCode, generate_ca_code  # noqa: F401
 from .errors import (  # noqa: F401
+    FormatError,
     GnssPerfError,
     InvalidInputError,
     PipelineError,

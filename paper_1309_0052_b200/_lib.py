@@ -44,8 +44,9 @@ class Stats(C.Structure):
 ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
 
 EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
-           "gacq_run", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset", "gacq_host_alloc",
-           "gacq_host_free", "gacq_ca_code")
+           "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
+           "gacq_host_alloc", "gacq_host_free", "gacq_ca_code")
+FMT_INT8, FMT_INT16 = 0, 1
 
 
 def _load() -> C.CDLL:
@@ -60,6 +61,8 @@ def _load() -> C.CDLL:
     lib.gacq_destroy.argtypes = [C.c_void_p]
     lib.gacq_destroy.restype = None
     lib.gacq_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_uint32, C.c_void_p]
+    lib.gacq_run_quantized.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_int64, C.c_int64,
+                                       C.c_uint32, C.c_void_p]
     lib.gacq_power_map.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.gacq_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]
     lib.gacq_stats_reset.argtypes = [C.c_void_p]

@@ -247,6 +247,47 @@ class AcqEngine:
     def search(self, snapshots, profile: bool = False) -> BatchResult:
         return self.finish(self.run_rows(snapshots, profile=profile))
 
+    def run_rows_quantized(self, iq, sample_format: int, scale: float, per_bin: bool = False,
+                           profile: bool = False) -> np.ndarray:
+        """Search integer I/Q snapshots (the IF-file payload, iffile.py:74-99) without a host
+        dequantization: `iq` is int8/int16 [n_snap, 2*L] interleaved I/Q (host array, or a CUDA
+        array via __cuda_array_interface__); the device applies float32(float64(q)*scale/limit)."""
+        if sample_format not in (_lib.FMT_INT8, _lib.FMT_INT16):
+            raise InvalidInputError(f"unknown sample format {sample_format!r}")
+        want = np.dtype(np.int8 if sample_format == _lib.FMT_INT8 else np.int16)
+        flags = (_lib.ROWS_PER_BIN if per_bin else 0) | (_lib.PROFILE if profile else 0)
+        cai = getattr(iq, "__cuda_array_interface__", None)
+        if cai is not None:
+            if np.dtype(cai["typestr"]) != want:
+                raise InvalidInputError(f"device I/Q must be {want}, got {cai['typestr']}")
+            shape = tuple(cai["shape"])
+            shape = (1, shape[0]) if len(shape) == 1 else shape
+            strides = cai.get("strides")
+            if strides and len(strides) == 2 and strides[1] != want.itemsize:
+                raise InvalidInputError("device I/Q must be contiguous along samples")
+            row = strides[0] // want.itemsize if strides and len(strides) == 2 else shape[1]
+            ptr = cai["data"][0]
+            flags |= _lib.SNAPS_ON_DEVICE
+        else:
+            arr = np.asarray(iq)
+            if arr.dtype != want:
+                raise InvalidInputError(f"I/Q must be {want}, got {arr.dtype}")
+            arr = np.ascontiguousarray(arr[None, :] if arr.ndim == 1 else arr)
+            shape, row, ptr = arr.shape, arr.shape[1], arr.ctypes.data
+        n_snap, n_vals = shape
+        if n_vals % 2 or row % 2:
+            raise InvalidInputError("interleaved I/Q needs an even number of values per snapshot")
+        if n_vals // 2 < self.span:
+            raise InvalidInputError(f"buffer holds {n_vals // 2} samples, {self.span} needed for the "
+                                    "configured integration")
+        out = np.empty((n_snap, self.prns.size) + ((self.bins.size,) if per_bin else ()), dtype=_lib.ROW_DTYPE)
+        _lib.check(_lib.lib.gacq_run_quantized(self._ctx, ptr, int(sample_format), float(scale), n_snap, row // 2,
+                                               flags, out.ctypes.data))
+        return out
+
+    def search_quantized(self, iq, sample_format: int, scale: float, profile: bool = False) -> BatchResult:
+        return self.finish(self.run_rows_quantized(iq, sample_format, scale, profile=profile))
+
     def power_map(self, snapshot) -> np.ndarray:
         """float32 [n_prn, n_bins, P] noncoherent power of one host snapshot (parity hook)."""
         arr = _host_array(snapshot)
@@ -381,3 +422,32 @@ def acquire_batch(snapshots, sample_rate_hz: float, prns, config: AcqConfig | No
     if errs:
         raise errs[0]
     return [r for o in outs for r in o]
+
+
+def acquire_if_file(path, prns, config: AcqConfig | None = None, device: int = 0) -> list:
+    """The CLI `acquire` path (cli.py:164-169: read_if_file -> acquire_all) with the
+    dequantization fused into the device pipeline for integer formats."""
+    from .iffile import FORMAT_FLOAT32, read_if_payload
+
+    config = config or AcqConfig()
+    payload = read_if_payload(path)
+    if payload.sample_format == FORMAT_FLOAT32:
+        return acquire_all(payload.to_iq_buffer(), list(prns), config, device=device)
+    if not prns:
+        raise InvalidInputError("prns must be non-empty")
+    if len(set(prns)) != len(prns):
+        raise InvalidInputError("prns must be distinct")
+    fs = payload.sample_rate_hz
+    n = payload.n_samples
+    n_coh = round(fs * config.coherent_ms * 1e-3)
+    period = samples_per_code_period(fs)
+    try:
+        if n < period:
+            raise InvalidInputError("buffer shorter than one code period")
+        if n < n_coh * config.noncoherent_rounds:
+            raise InvalidInputError(f"buffer holds {n} samples, "
+                                    f"{n_coh * config.noncoherent_rounds} needed for the configured integration")
+    except InvalidInputError as exc:
+        raise PipelineError(prns[0], repr(exc)) from exc
+    eng = get_engine(fs, list(prns), config, device)
+    return eng.search_quantized(payload.iq, payload.sample_format, payload.scale).results()[0]

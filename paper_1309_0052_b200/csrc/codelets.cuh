@@ -26,18 +26,8 @@ __device__ __forceinline__ cx pk(float re, float im) {
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(re), "f"(im));
     return r;
 }
-__device__ __forceinline__ float re(cx v) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-    (void)b;
-    return a;
-}
-__device__ __forceinline__ float im(cx v) {
-    float a, b;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-    (void)a;
-    return b;
-}
+__device__ __forceinline__ float re(cx v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float im(cx v) { return __uint_as_float((unsigned)(v >> 32)); }
 __device__ __forceinline__ cx bc(float x) { return pk(x, x); }
 __device__ __forceinline__ cx czero() { return 0ull; }
 

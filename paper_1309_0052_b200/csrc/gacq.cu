@@ -125,7 +125,9 @@ struct gacq_ctx {
     float4* d_Z = nullptr;
     int64_t z_pairs = 0;  // pairs per chunk that fit in the scratch
     float2* d_in = nullptr;
-    int64_t in_cap = 0;   // snapshots
+    int64_t in_cap = 0;   // complex64 staging (samples)
+    char* d_raw = nullptr;
+    int64_t raw_cap = 0;  // quantized H2D staging (bytes)
     gacq_row* d_rows_bin = nullptr;
     int64_t rows_bin_cap = 0;
     gacq_row* d_rows = nullptr;
@@ -211,12 +213,43 @@ cudaEvent_t prof_event(gacq_ctx* c, size_t i) {
     return c->prof_events[i];
 }
 
-// Core pipeline. `src` is a device pointer when on_device, else a host pointer.
-int run_impl(gacq_ctx* c, const float2* src, int64_t n_snap, int64_t stride, bool on_device, bool per_bin,
-             bool profile, gacq_row* rows_out, bool rows_on_device, float* pmap) {
+// Snapshot batch as handed to gacq_run / gacq_run_quantized.
+struct Input {
+    const void* ptr;
+    int fmt;         // kFmtComplex64, or GACQ_FMT_INT8 / GACQ_FMT_INT16 interleaved I/Q
+    double scale;    // full-scale amplitude of integer formats (iffile.py:32-43)
+    bool on_device;
+    int64_t stride;  // samples (I/Q pairs) between snapshot starts
+};
+constexpr int kFmtComplex64 = -1;
+
+int sample_bytes(int fmt) { return fmt == GACQ_FMT_INT8 ? 2 : fmt == GACQ_FMT_INT16 ? 4 : (int)sizeof(float2); }
+
+// integer I/Q -> complex64 exactly as read_if_file: float32(float64(q) * (scale / limit))
+// (iffile.py:95-98; limit 127 / 32767, iffile.py:43)
+cudaError_t launch_dequant(const gacq_ctx* c, const Input& in, int64_t s0, int64_t ns, const void* src,
+                           int64_t src_stride, float2* dst, int64_t span) {
+    const double s = in.scale / (in.fmt == GACQ_FMT_INT8 ? 127.0 : 32767.0);
+    const int64_t n = ns * span;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    if (in.fmt == GACQ_FMT_INT8)
+        gacq_dequant_kernel<int8_t><<<blocks, 256, 0, c->copy_stream>>>(
+            (const int8_t*)src, src_stride, reinterpret_cast<cx*>(dst), span, n, s);
+    else
+        gacq_dequant_kernel<int16_t><<<blocks, 256, 0, c->copy_stream>>>(
+            (const int16_t*)src, src_stride, reinterpret_cast<cx*>(dst), span, n, s);
+    (void)s0;
+    return cudaGetLastError();
+}
+
+// Core pipeline. `in.ptr` is a device pointer when in.on_device, else a host pointer.
+int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool profile, gacq_row* rows_out,
+             bool rows_on_device, float* pmap) {
     const int64_t span = (int64_t)c->R * c->n_coh;
     const int64_t n_pairs = n_snap * c->B;
     const int64_t n_rows = n_snap * c->n_prn;
+    const bool quantized = inp.fmt != kFmtComplex64;
+    const bool staged = !inp.on_device || quantized;
     int rc;
     if ((rc = grow(&c->d_rows_bin, &c->rows_bin_cap, n_rows * c->B))) return rc;
     if (!per_bin && (rc = grow(&c->d_rows, &c->rows_cap, n_rows))) return rc;
@@ -225,14 +258,17 @@ int run_impl(gacq_ctx* c, const float2* src, int64_t n_snap, int64_t stride, boo
     if (profile) {
         run_start = prof_event(c, 0);
         run_end = prof_event(c, 1);
-        CUDA_TRY(cudaEventRecord(run_start, on_device ? c->stream : c->copy_stream));
+        CUDA_TRY(cudaEventRecord(run_start, staged ? c->copy_stream : c->stream));
     }
-    const float2* in = src;
-    int64_t in_stride = stride;
-    // H2D in snapshot chunks on the copy stream; chunk k is covered by copy_events[k]
+    const float2* in = (const float2*)inp.ptr;
+    int64_t in_stride = inp.stride;
+    // Staging in snapshot chunks on the copy stream (H2D and/or dequantization);
+    // chunk k is covered by copy_events[k]
     int64_t copy_chunk = 0, n_copy_chunks = 0;
-    if (!on_device) {
+    if (staged) {
         if ((rc = grow(&c->d_in, &c->in_cap, n_snap * span))) return rc;
+        const int64_t sb = sample_bytes(inp.fmt);
+        if (quantized && !inp.on_device && (rc = grow(&c->d_raw, &c->raw_cap, n_snap * span * sb))) return rc;
         in = c->d_in;
         in_stride = span;
         copy_chunk = std::max<int64_t>(1, std::min<int64_t>(n_snap, c->z_pairs / c->B));
@@ -242,15 +278,27 @@ int run_impl(gacq_ctx* c, const float2* src, int64_t n_snap, int64_t stride, boo
             CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             c->copy_events.push_back(e);
         }
+        const char* src = (const char*)inp.ptr;
         for (int64_t k = 0; k < n_copy_chunks; ++k) {
             const int64_t s0 = k * copy_chunk, ns = std::min(copy_chunk, n_snap - s0);
-            CUDA_TRY(cudaMemcpy2DAsync(c->d_in + s0 * span, span * sizeof(float2), src + s0 * stride,
-                                       stride * sizeof(float2), span * sizeof(float2), ns,
-                                       cudaMemcpyHostToDevice, c->copy_stream));
+            if (!quantized) {
+                CUDA_TRY(cudaMemcpy2DAsync(c->d_in + s0 * span, span * sb, src + s0 * inp.stride * sb,
+                                           inp.stride * sb, span * sb, ns, cudaMemcpyHostToDevice, c->copy_stream));
+            } else if (!inp.on_device) {
+                CUDA_TRY(cudaMemcpy2DAsync(c->d_raw + s0 * span * sb, span * sb, src + s0 * inp.stride * sb,
+                                           inp.stride * sb, span * sb, ns, cudaMemcpyHostToDevice, c->copy_stream));
+                CUDA_TRY(launch_dequant(c, inp, s0, ns, c->d_raw + s0 * span * sb, span, c->d_in + s0 * span, span));
+                c->stats.launches++;
+            } else {
+                CUDA_TRY(launch_dequant(c, inp, s0, ns, src + s0 * inp.stride * sb, inp.stride, c->d_in + s0 * span,
+                                        span));
+                c->stats.launches++;
+            }
             CUDA_TRY(cudaEventRecord(c->copy_events[k], c->copy_stream));
         }
-        c->stats.h2d_bytes += n_snap * span * (int64_t)sizeof(float2);
+        if (!inp.on_device) c->stats.h2d_bytes += n_snap * span * sb;
     }
+    const bool on_device = !staged;
 
     size_t ev = 2;
     int64_t waited = -1;
@@ -328,6 +376,7 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_tw);
         cudaFree(c->d_Z);
         cudaFree(c->d_in);
+        cudaFree(c->d_raw);
         cudaFree(c->d_rows_bin);
         cudaFree(c->d_rows);
         cudaFree(c->d_pmap);
@@ -476,8 +525,12 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
-    const int fsm = fwd_smem_bytes(c), csm = corr_smem_bytes(c);
-    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, csm));
+    // Function attributes are process-wide (shared by every plan), so each kernel gets the
+    // largest dynamic shared memory any plan can launch it with -- a function of its
+    // template parameters only, never of this plan.
+    const int csm = corr_smem_bytes(c);
+    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(float) * 4 * kRow));
     CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     {
@@ -492,8 +545,9 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     if (!corr_row_in_smem(c))
         CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kRow * sizeof(float)));
     CTX_TRY(cudaMalloc(&c->d_counter, sizeof(unsigned long long)));
-#define GACQ_ATTR_FWD(NG, DM) \
-    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<NG, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm));
+#define GACQ_ATTR_FWD(NG, DM)                                                                 \
+    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<NG, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)sizeof(float2) * (DM * fwd_ws(DM) + NG * 2 * kXchg)));
     GACQ_FWD_VARIANTS(GACQ_ATTR_FWD)
 #undef GACQ_ATTR_FWD
 
@@ -527,8 +581,28 @@ int gacq_run(gacq_ctx* c, const void* snaps, int64_t n_snap, int64_t stride, uin
                     (long long)span);
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
-    return run_impl(c, (const float2*)snaps, n_snap, std::max(stride, span), flags & GACQ_SNAPS_ON_DEVICE,
-                    flags & GACQ_ROWS_PER_BIN, flags & GACQ_PROFILE, rows, flags & GACQ_ROWS_ON_DEVICE, nullptr);
+    const Input in{snaps, kFmtComplex64, 1.0, (flags & GACQ_SNAPS_ON_DEVICE) != 0, std::max(stride, span)};
+    return run_impl(c, in, n_snap, flags & GACQ_ROWS_PER_BIN, flags & GACQ_PROFILE, rows, flags & GACQ_ROWS_ON_DEVICE,
+                    nullptr);
+}
+
+int gacq_run_quantized(gacq_ctx* c, const void* iq, int32_t sample_format, double scale, int64_t n_snap,
+                       int64_t stride, uint32_t flags, gacq_row* rows) {
+    if (!c) return fail(GACQ_ERR_INVALID, "null context");
+    if (n_snap < 1) return fail(GACQ_ERR_INVALID, "n_snap must be >= 1");
+    if (!iq || !rows) return fail(GACQ_ERR_INVALID, "null buffer");
+    if (sample_format != GACQ_FMT_INT8 && sample_format != GACQ_FMT_INT16)
+        return fail(GACQ_ERR_INVALID, "unknown sample format %d", sample_format);
+    if (!std::isfinite(scale)) return fail(GACQ_ERR_INVALID, "scale must be finite");
+    const int64_t span = (int64_t)c->R * c->n_coh;
+    if (stride < span && n_snap > 1)
+        return fail(GACQ_ERR_INVALID, "stride %lld < %lld samples needed per snapshot", (long long)stride,
+                    (long long)span);
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    const Input in{iq, sample_format, scale, (flags & GACQ_SNAPS_ON_DEVICE) != 0, std::max(stride, span)};
+    return run_impl(c, in, n_snap, flags & GACQ_ROWS_PER_BIN, flags & GACQ_PROFILE, rows, flags & GACQ_ROWS_ON_DEVICE,
+                    nullptr);
 }
 
 int gacq_power_map(gacq_ctx* c, const void* snap, float* out) {
@@ -541,7 +615,8 @@ int gacq_power_map(gacq_ctx* c, const void* snap, float* out) {
         return fail(GACQ_ERR_RESOURCE, "cudaMalloc power map failed");
     }
     const int64_t span = (int64_t)c->R * c->n_coh;
-    int rc = run_impl(c, (const float2*)snap, 1, span, false, true, false, nullptr, false, c->d_pmap);
+    const Input in{snap, kFmtComplex64, 1.0, false, span};
+    int rc = run_impl(c, in, 1, true, false, nullptr, false, c->d_pmap);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpy(out, c->d_pmap, n * sizeof(float), cudaMemcpyDeviceToHost));
     return GACQ_OK;

@@ -450,6 +450,19 @@ __global__ void __launch_bounds__(kT, GACQ_CORR_MIN_BLOCKS) gacq_corr_kernel(Cor
     }
 }
 
+// Integer I/Q -> complex64, bit-identical to read_if_file (iffile.py:95-98):
+// float32(float64(q) * s) per component with s = scale / limit computed on the host.
+// n = snapshots * span samples; snapshot j's sample k sits at src[2 (j*src_stride + k)].
+template <typename T>
+__global__ void gacq_dequant_kernel(const T* __restrict__ src, int64_t src_stride, cx* __restrict__ dst,
+                                    int64_t span, int64_t n, double s) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = i / span, k = i - j * span;
+        const T* q = src + 2 * (j * src_stride + k);
+        dst[i] = pk((float)((double)q[0] * s), (float)((double)q[1] * s));
+    }
+}
+
 // one warp per (snapshot, prn): merge bin rows -- np.argmax order (acquisition.py:151):
 // highest peak, ties -> lowest bin (the row's own first lag is already the lowest)
 __global__ void gacq_reduce_kernel(const gacq_row* __restrict__ rows_bin, gacq_row* __restrict__ rows,

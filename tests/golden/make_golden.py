@@ -210,6 +210,21 @@ def main():
                                      doppler_span_hz=9750.0, truth=truth), buf,
         [t[0] for t in truth[:5]] + [p for p in all_prns if p not in [t[0] for t in truth]][:3],
         C4)
+    # IF files (iffile.py): the reference writes a C3 snapshot as int8 / int16 / float32 and
+    # acquires what read_if_file gives back (the cli.py:164-169 acquire path)
+    import tempfile
+
+    from gnssperf.iffile import read_if_file, write_if_file
+
+    buf, truth = ref_snapshot(2, fs4, 10e-3, base_seed=300)
+    for fmt in ("int8", "int16", "float32"):
+        with tempfile.TemporaryDirectory() as td:
+            path = Path(td) / f"snap.{fmt}.gnssif"
+            write_if_file(path, buf, fmt)
+            file_sha = hashlib.sha256(path.read_bytes()).hexdigest()
+            back = read_if_file(path)
+        add(f"if_{fmt}_c3", "iffile", dict(index=2, fs=fs4, duration_s=10e-3, base_seed=300, fmt=fmt,
+                                          file_sha256=file_sha, truth=truth), back, all_prns, C3)
 
     (OUT / "golden.json").write_text(json.dumps(dict(
         generator="tests/golden/make_golden.py", reference="gnssperf 0.1.0 (/root/reference/pkg)",

@@ -1,0 +1,77 @@
+"""GPU parity of the IF-ingest path: integer I/Q payloads are
+dequantized on the device (float32(float64(q) * scale/limit), iffile.py:95-98) and must give
+the reference's read_if_file -> acquire_all results."""
+
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from golden_cases import case, if_bytes, if_decoded, load_cases
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+IF_CASES = [c["name"] for c in load_cases() if c["kind"] == "iffile"]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1309_0052_b200 import build
+
+    build.build()
+    import paper_1309_0052_b200 as p
+
+    return p
+
+
+def check(results, c):
+    for g, r in zip(results, c["results"]):
+        gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples,
+                  peak_metric=g.peak_metric, detected=g.detected)
+        assert g.prn == r["prn"]
+        assert compare(gd, r, c["config"]["detection_threshold"]) == "exact", (c["name"], g, r)
+
+
+@pytest.mark.parametrize("name", IF_CASES)
+def test_acquire_if_file_matches_reference(pkg, name):
+    c = case(name)
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "snap.gnssif"
+        p.write_bytes(if_bytes(c))
+        res = pkg.acquire_if_file(p, c["prns"], pkg.AcqConfig(**c["config"]))
+    check(res, c)
+
+
+@pytest.mark.parametrize("name", [n for n in IF_CASES if "float32" not in n])
+def test_quantized_rows_equal_host_dequantized_rows(pkg, name):
+    # device dequantization is bit-identical to read_if_file, so the rows must be identical
+    c = case(name)
+    fs, samples, fmt, scale, ints = if_decoded(c)
+    eng = pkg.get_engine(fs, c["prns"], pkg.AcqConfig(**c["config"]))
+    rows_q = eng.run_rows_quantized(ints, fmt, scale)
+    rows_f = eng.run_rows(samples)
+    np.testing.assert_array_equal(rows_q, rows_f)
+
+
+def test_quantized_batch_strided_and_device(pkg):
+    import torch
+
+    c = case("if_int8_c3")
+    fs, samples, fmt, scale, ints = if_decoded(c)
+    eng = pkg.get_engine(fs, c["prns"], pkg.AcqConfig(**c["config"]))
+    one = eng.run_rows_quantized(ints, fmt, scale)
+    wide = np.zeros((3, ints.size + 64), dtype=np.int8)
+    wide[:, :ints.size] = ints
+    np.testing.assert_array_equal(eng.run_rows_quantized(wide, fmt, scale), np.repeat(one, 3, axis=0))
+    dev = torch.from_numpy(wide).cuda()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(eng.run_rows_quantized(dev, fmt, scale), np.repeat(one, 3, axis=0))
+    st = eng.stats()
+    assert st["launches"] > 0
+    with pytest.raises(pkg.InvalidInputError):
+        eng.run_rows_quantized(ints.astype(np.int16), fmt, scale)

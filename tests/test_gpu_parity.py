@@ -196,3 +196,17 @@ def test_c5_weak_signal_sweep_decisions(pkg, cn0):
             exact += v == "exact"
             ties += v == "tie"
     assert exact >= 4 * 32 - 1, (exact, ties)
+
+
+def test_plans_with_different_rates_coexist(pkg):
+    """Kernel attributes are process-wide: creating a D=2 plan after a D=4 one must not
+    break the D=4 plan (regression: launch 'invalid argument')."""
+    cfg = pkg.AcqConfig(doppler_step_hz=500.0, noncoherent_rounds=1)
+    rates = (4.092e6, 2.046e6, 16.368e6, 8.184e6)
+    engines = [pkg.AcqEngine(fs, [1, 2], cfg) for fs in rates]
+    for fs, eng in zip(rates, engines):
+        x = oracle.make_snapshot(0, fs, 1e-3, base_seed=31)[0]
+        rows = eng.run_rows(x)
+        assert rows.shape == (1, 2)
+    for eng in engines:
+        eng.close()

@@ -66,3 +66,35 @@ def test_ca_codes_balanced_and_distinct():
     assert len({c.tobytes() for c in codes}) == 32
     with pytest.raises(ValueError):
         oracle.generate_ca_code(33)
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in load_cases() if c["kind"] == "iffile"])
+def test_if_files_match_reference_bytes(name):
+    from golden_cases import if_bytes
+
+    import hashlib
+
+    c = case(name)
+    raw = if_bytes(c)
+    assert hashlib.sha256(raw).hexdigest() == c["spec"]["file_sha256"]
+    # the product's writer / reader mirror the reference byte for byte
+    import paper_1309_0052_b200 as g
+
+    _, samples, _, _, _ = oracle.if_file_decode(raw)
+    assert sha(samples) == c["input_sha256"]
+    import tempfile
+    from pathlib import Path
+
+    with tempfile.TemporaryDirectory() as td:
+        p = Path(td) / "x.gnssif"
+        p.write_bytes(raw)
+        buf = g.read_if_file(p)
+        assert sha(buf.samples) == c["input_sha256"]
+        q = Path(td) / "y.gnssif"
+        g.write_if_file(q, g.IqBuffer._wrap(oracle.make_snapshot(
+            c["spec"]["index"], c["spec"]["fs"], c["spec"]["duration_s"], c["spec"]["base_seed"])[0],
+            c["spec"]["fs"], g.Precision.SINGLE), c["spec"]["fmt"])
+        assert q.read_bytes() == raw
+        with pytest.raises(g.FormatError):
+            (Path(td) / "bad").write_bytes(b"NOTGNSS!" + raw[8:])
+            g.read_if_file(Path(td) / "bad")
