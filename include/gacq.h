@@ -135,6 +135,33 @@ int gacq_power_map(gacq_ctx* ctx, const void* snap_host, float* out_host);
 int gacq_stats_get(const gacq_ctx* ctx, gacq_stats* out);
 int gacq_stats_reset(gacq_ctx* ctx);
 
+/* ---- Tracking correlators ------------------------------------
+ * Replaces epl_correlate (tracking.py:126-165) for a batch of channels: carrier wipe-off
+ * with the 48-bit NCO (kernels.py:106-114, fp64 cos/sin rounded to complex64, bit-exact
+ * complex64 product) and the three E/P/L dot products against floor-indexed code replicas
+ * of the 42-bit code NCO (kernels.py:116-128). The fixed-point starts and steps are given
+ * per channel exactly as the reference computes them (kernels.py:56-70), so the replicas
+ * are bit-identical; the dot products accumulate in float64 and round to float32 once
+ * (the reference accumulates left to right in complex64: results agree to ~1e-6). */
+typedef struct gacq_epl_chan {
+    int64_t block_offset;  /* complex samples from `blocks` to this channel's first sample */
+    uint64_t carrier_p0;   /* carrier_phase_to_fixed(state.carrier_phase_cycles)           */
+    uint64_t carrier_step; /* carrier_step_to_fixed(state.doppler_hz, fs)                  */
+    uint64_t code_p0[3];   /* code_phase_to_fixed((phase + {+d/2, 0, -d/2}) % 1023)        */
+    uint64_t code_step;    /* code_step_to_fixed(state.code_rate_hz, fs)                   */
+    int32_t prn;           /* 1..32                                                         */
+    int32_t reserved;
+} gacq_epl_chan;
+
+typedef struct gacq_trk gacq_trk;
+int gacq_trk_create(gacq_trk** out, int32_t device);
+void gacq_trk_destroy(gacq_trk* trk);
+/* out[c*6 + 0..5] = (ie, qe, ip, qp, il, ql) of channel c over n_samples samples.
+ * `blocks` holds total_samples complex64 samples (host, or device with
+ * GACQ_SNAPS_ON_DEVICE); every channel's block must lie inside it. */
+int gacq_trk_epl(gacq_trk* trk, const void* blocks, int64_t total_samples, int32_t n_samples,
+                 const gacq_epl_chan* chans, int64_t n_chan, uint32_t flags, float* out);
+
 /* Page-locked host buffers for overlapped H2D (cudaHostAlloc / cudaFreeHost). */
 int gacq_host_alloc(int64_t bytes, void** out);
 int gacq_host_free(void* ptr);

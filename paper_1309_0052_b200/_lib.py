@@ -45,7 +45,8 @@ ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
 
 EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
            "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
-           "gacq_host_alloc", "gacq_host_free", "gacq_ca_code")
+           "gacq_host_alloc", "gacq_host_free", "gacq_ca_code", "gacq_trk_create", "gacq_trk_destroy",
+           "gacq_trk_epl")
 FMT_INT8, FMT_INT16 = 0, 1
 
 
@@ -69,6 +70,11 @@ def _load() -> C.CDLL:
     lib.gacq_host_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]
     lib.gacq_host_free.argtypes = [C.c_void_p]
     lib.gacq_ca_code.argtypes = [C.c_int32, C.c_void_p]
+    lib.gacq_trk_create.argtypes = [C.POINTER(C.c_void_p), C.c_int32]
+    lib.gacq_trk_destroy.argtypes = [C.c_void_p]
+    lib.gacq_trk_destroy.restype = None
+    lib.gacq_trk_epl.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_uint32,
+                                 C.c_void_p]
     if lib.gacq_version() != 1:
         raise ImportError("libgacq ABI version mismatch")
     return lib

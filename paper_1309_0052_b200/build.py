@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB = PKG / "libgacq.so"
 SOURCES = [PKG / "csrc" / "gacq.cu"]
-DEPS = SOURCES + [PKG / "csrc" / "gacq_kernels.cuh", PKG / "csrc" / "codelets.cuh",
+DEPS = SOURCES + [PKG / "csrc" / "gacq_kernels.cuh", PKG / "csrc" / "codelets.cuh", PKG / "csrc" / "gtrk_kernels.cuh",
                   ROOT / "include" / "gacq.h"]
 
 

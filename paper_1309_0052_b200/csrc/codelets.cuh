@@ -61,11 +61,13 @@ __device__ __forceinline__ cx rot(cx a) {
 __device__ __forceinline__ cx cmul(cx a, cx w) { return fma2(rot<1>(a), bc(im(w)), mul2(a, bc(re(w)))); }
 __device__ __forceinline__ float cmag2(cx a) { return re(a) * re(a) + im(a) * im(a); }
 
-// exact complex64 product of kernels.py:78-86: round(ar*br) -/+ round(ai*bi) etc., no FMA
+// exact complex64 product of kernels.py:78-86: round(round(ar*br) - round(ai*bi)),
+// round(round(ar*bi) + round(ai*br)). Scalar __fmul_rn/__fadd_rn are never contracted;
+// ptxas DOES fuse mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (observed in SASS), so the
+// packed forms must not be used here.
 __device__ __forceinline__ cx cmul_exact(cx a, cx b) {
-    const cx t1 = mul2(a, bc(re(b)));                  // (ar*br, ai*br)
-    const cx t2 = mul2(pk(im(a), re(a)), bc(im(b)));   // (ai*bi, ar*bi)
-    return add2(t1, pk(-re(t2), im(t2)));              // (ar*br - ai*bi, ai*br + ar*bi)
+    const float ar = re(a), ai = im(a), br = re(b), bi = im(b);
+    return pk(__fsub_rn(__fmul_rn(ar, br), __fmul_rn(ai, bi)), __fadd_rn(__fmul_rn(ar, bi), __fmul_rn(ai, br)));
 }
 
 constexpr float kC8 = 0.70710678118654752440f;  // cos(pi/4)

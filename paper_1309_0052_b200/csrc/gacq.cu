@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "gacq_kernels.cuh"
+#include "gtrk_kernels.cuh"
 
 using namespace gacq;
 
@@ -647,6 +648,100 @@ int gacq_stats_reset(gacq_ctx* c) {
     if (!c) return fail(GACQ_ERR_INVALID, "null argument");
     std::lock_guard<std::mutex> lk(c->mu);
     c->stats = gacq_stats{};
+    return GACQ_OK;
+}
+
+// ---- tracking correlators ----------------------------------------------------------
+
+struct gacq_trk {
+    std::mutex mu;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int8_t* d_chips = nullptr;  // [32][1024] +/-1
+    float2* d_blocks = nullptr;
+    int64_t blocks_cap = 0;
+    gacq_epl_chan* d_chans = nullptr;
+    int64_t chans_cap = 0;
+    float* d_out = nullptr;
+    int64_t out_cap = 0;
+};
+
+static void trk_free(gacq_trk* t) {
+    if (!t) return;
+    {
+        DeviceGuard g(t->device);
+        if (t->stream) cudaStreamSynchronize(t->stream);
+        cudaFree(t->d_chips);
+        cudaFree(t->d_blocks);
+        cudaFree(t->d_chans);
+        cudaFree(t->d_out);
+        if (t->stream) cudaStreamDestroy(t->stream);
+    }
+    delete t;
+}
+
+int gacq_trk_create(gacq_trk** out, int32_t device) {
+    if (!out) return fail(GACQ_ERR_INVALID, "null argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(GACQ_ERR_CUDA, "no CUDA device visible");
+    }
+    if (device < 0 || device >= ndev) return fail(GACQ_ERR_INVALID, "device %d out of range", device);
+    gacq_trk* t = new gacq_trk();
+    t->device = device;
+    std::vector<int8_t> chips(32 * 1024, 0);
+    for (int p = 1; p <= 32; ++p) ca_code(p, chips.data() + (p - 1) * 1024);
+    DeviceGuard g(device);
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(gacq_epl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kTrkMaxSmem)) != cudaSuccess ||
+        (e = cudaMalloc(&t->d_chips, chips.size())) != cudaSuccess ||
+        (e = cudaMemcpy(t->d_chips, chips.data(), chips.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+        trk_free(t);
+        return fail(GACQ_ERR_CUDA, "tracker setup failed: %s", cudaGetErrorString(e));
+    }
+    *out = t;
+    return GACQ_OK;
+}
+
+void gacq_trk_destroy(gacq_trk* t) { trk_free(t); }
+
+int gacq_trk_epl(gacq_trk* t, const void* blocks, int64_t total, int32_t n, const gacq_epl_chan* chans,
+                 int64_t n_chan, uint32_t flags, float* out) {
+    if (!t || !blocks || !chans || !out) return fail(GACQ_ERR_INVALID, "null argument");
+    if (n < 1 || n_chan < 1 || total < n) return fail(GACQ_ERR_INVALID, "bad sizes");
+    const int smem = n * (int)(sizeof(float2) + 3);
+    if (smem > kTrkMaxSmem)
+        return fail(GACQ_ERR_UNSUPPORTED, "tracking block of %d samples exceeds one CTA's shared memory", n);
+    for (int64_t i = 0; i < n_chan; ++i) {
+        if (chans[i].prn < 1 || chans[i].prn > 32)
+            return fail(GACQ_ERR_INVALID, "prn must be an integer in 1..32, got %d", chans[i].prn);
+        if (chans[i].block_offset < 0 || chans[i].block_offset + n > total)
+            return fail(GACQ_ERR_INVALID, "channel %lld block outside the sample buffer", (long long)i);
+        if (chans[i].carrier_p0 >> 48 || chans[i].carrier_step >> 48 || chans[i].code_step >= kCodeMod ||
+            chans[i].code_p0[0] >= kCodeMod || chans[i].code_p0[1] >= kCodeMod || chans[i].code_p0[2] >= kCodeMod)
+            return fail(GACQ_ERR_INVALID, "channel %lld NCO word out of range", (long long)i);
+    }
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    const float2* x = (const float2*)blocks;
+    int rc;
+    if (!(flags & GACQ_SNAPS_ON_DEVICE)) {
+        if ((rc = grow(&t->d_blocks, &t->blocks_cap, total))) return rc;
+        CUDA_TRY(cudaMemcpyAsync(t->d_blocks, blocks, total * sizeof(float2), cudaMemcpyHostToDevice, t->stream));
+        x = t->d_blocks;
+    }
+    if ((rc = grow(&t->d_chans, &t->chans_cap, n_chan))) return rc;
+    if ((rc = grow(&t->d_out, &t->out_cap, n_chan * 6))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(t->d_chans, chans, n_chan * sizeof(gacq_epl_chan), cudaMemcpyHostToDevice, t->stream));
+    gacq_epl_kernel<<<(unsigned)n_chan, kTrkThreads, smem, t->stream>>>(reinterpret_cast<const cx*>(x), n,
+                                                                          t->d_chans, t->d_chips, t->d_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, t->d_out, n_chan * 6 * sizeof(float), cudaMemcpyDeviceToHost, t->stream));
+    CUDA_TRY(cudaStreamSynchronize(t->stream));
     return GACQ_OK;
 }
 

@@ -1,0 +1,300 @@
+"""Tracking channels -- drop-in for gnssperf/tracking.py.
+
+The receiver's step after acquisition. The O(N) per-epoch work -- carrier wipe-off plus
+the early / prompt / late dot products (tracking.py:126-165) -- runs on the GPU for a whole
+batch of channels in one launch (libgacq ``gacq_trk_epl``); the scalar loop math
+(discriminators, second-order loop filters, fixed-point NCO advance, lock detector,
+tracking.py:168-275) stays on the host in float64 with the reference's formulas.
+
+Replicas are bit-identical to the reference's (the fixed-point NCO words are computed here
+with kernels.py's exact expressions); the dot products accumulate in float64 on the device
+instead of the reference's left-to-right complex64 sum, so correlators agree to ~1e-6
+relative and the loop states to the same order.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib
+from .cacode import CHIP_RATE_HZ, CODE_LENGTH
+from .errors import DegenerateInputError, InvalidConfigError, InvalidInputError
+
+L1_CARRIER_HZ = 1575.42e6  # gnss_signal.py:34
+LOOP_DAMPING = 0.7071067811865476  # tracking.py:44
+LOCK_SMOOTHING_EPOCHS = 20  # tracking.py:45
+
+CARRIER_SCALE = 1 << 48  # kernels.py:47-50
+CODE_SCALE = 1 << 42  # kernels.py:52-53
+CODE_MODULUS = CODE_LENGTH * CODE_SCALE
+
+
+def carrier_phase_to_fixed(phase_cycles: float) -> int:  # kernels.py:56-58
+    return int(round((phase_cycles % 1.0) * CARRIER_SCALE)) % CARRIER_SCALE
+
+
+def carrier_step_to_fixed(freq_hz: float, fs: float) -> int:  # kernels.py:61-62
+    return int(round((freq_hz / fs) * CARRIER_SCALE)) % CARRIER_SCALE
+
+
+def code_phase_to_fixed(phase_chips: float) -> int:  # kernels.py:65-66
+    return int(round((phase_chips % 1023.0) * CODE_SCALE)) % CODE_MODULUS
+
+
+def code_step_to_fixed(chip_rate_hz: float, fs: float) -> int:  # kernels.py:69-70
+    return int(round((chip_rate_hz / fs) * CODE_SCALE))
+
+
+@dataclass(frozen=True)
+class TrackConfig:
+    """tracking.py:48-67 (same validation and messages)."""
+
+    correlator_spacing_chips: float = 0.5
+    dll_bandwidth_hz: float = 2.0
+    pll_bandwidth_hz: float = 15.0
+    integration_ms: int = 1
+
+    def __post_init__(self):
+        if not 0 < self.correlator_spacing_chips <= 1:
+            raise InvalidConfigError("correlator spacing must be in (0, 1] chips")
+        if self.dll_bandwidth_hz <= 0 or self.pll_bandwidth_hz <= 0:
+            raise InvalidConfigError("loop bandwidths must be > 0")
+        if self.integration_ms < 1:
+            raise InvalidConfigError("integration_ms must be >= 1")
+        t = self.integration_ms * 1e-3
+        for bw in (self.dll_bandwidth_hz, self.pll_bandwidth_hz):
+            if bw * t >= 0.25:
+                raise InvalidConfigError(f"stability guard violated: bandwidth {bw} Hz x {t} s >= 0.25")
+
+
+@dataclass(frozen=True)
+class TrackState:
+    """tracking.py:70-82."""
+
+    prn: int
+    code_phase_chips: float
+    carrier_phase_cycles: float
+    doppler_hz: float
+    code_rate_hz: float
+    dll_filter_state: tuple = (0.0, 0.0)
+    pll_filter_state: tuple = (0.0, 0.0)
+    epoch: int = 0
+    sample_rate_hz: float = 8.184e6
+    lock_nbd: float = 0.0
+    lock_nbp: float = 0.0
+
+
+@dataclass(frozen=True)
+class TrackOutput:
+    """tracking.py:85-97."""
+
+    ie: float
+    qe: float
+    ip: float
+    qp: float
+    il: float
+    ql: float
+    dll_error_chips: float = 0.0
+    pll_error_cycles: float = 0.0
+    lock_metric: float = 0.0
+    multiplications: int = 0
+    direct_equivalent_multiplications: int = 0
+
+
+def init_from_acquisition(acq, fs: float) -> TrackState:
+    """tracking.py:100-119: code delay -> prompt replica start phase (nominal chip rate)."""
+    if not acq.detected:
+        raise InvalidInputError(f"PRN {acq.prn} was not detected; nothing to track")
+    cps = CHIP_RATE_HZ / fs
+    return TrackState(prn=acq.prn, code_phase_chips=(-acq.code_phase_samples * cps) % CODE_LENGTH,
+                      carrier_phase_cycles=0.0, doppler_hz=acq.doppler_hz,
+                      code_rate_hz=CHIP_RATE_HZ * (1.0 + acq.doppler_hz / L1_CARRIER_HZ), sample_rate_hz=fs)
+
+
+def block_length(state: TrackState, config: TrackConfig) -> int:  # tracking.py:122-123
+    return round(state.sample_rate_hz * config.integration_ms * 1e-3)
+
+
+def dll_discriminator(out: TrackOutput, spacing_chips: float = 0.5) -> float:  # tracking.py:168-176
+    e = out.ie * out.ie + out.qe * out.qe
+    l = out.il * out.il + out.ql * out.ql
+    if e + l == 0:
+        if out.ip == 0 and out.qp == 0:
+            raise DegenerateInputError("all correlators zero")
+        return 0.0
+    return (e - l) / (e + l) * (1.0 - spacing_chips / 2.0) / 2.0
+
+
+def pll_discriminator(out: TrackOutput) -> float:  # tracking.py:179-185
+    if out.ip == 0.0 and out.qp == 0.0:
+        raise DegenerateInputError("prompt correlator is zero")
+    if out.ip == 0.0:
+        return math.copysign(0.25, out.qp)
+    return math.atan(out.qp / out.ip) / (2.0 * math.pi)
+
+
+def loop_gains(bandwidth_hz: float) -> tuple:  # tracking.py:188-190
+    w0 = bandwidth_hz / 0.53
+    return 2.0 * LOOP_DAMPING * w0, w0 * w0
+
+
+def loop_filter(error: float, state: tuple, bandwidth_hz: float, integration_s: float) -> tuple:
+    """tracking.py:193-208: second-order PI; returns (rate correction, new state)."""
+    if bandwidth_hz * integration_s >= 0.25:
+        raise InvalidConfigError(f"stability guard violated: {bandwidth_hz} Hz x {integration_s} s >= 0.25")
+    g1, g2 = loop_gains(bandwidth_hz)
+    acc, prev = state
+    acc_new = acc + g2 * integration_s * (error + prev) / 2.0
+    return g1 * error + acc_new, (acc_new, error)
+
+
+def _advance_carrier(phase, doppler, fs, n, step_cycles):  # tracking.py:211-215
+    p0 = carrier_phase_to_fixed(phase)
+    step = carrier_step_to_fixed(doppler, fs)
+    return ((p0 + n * step + carrier_phase_to_fixed(step_cycles)) % CARRIER_SCALE) / CARRIER_SCALE
+
+
+def _advance_code(phase, rate, fs, n, step_chips):  # tracking.py:218-223
+    p0 = code_phase_to_fixed(phase)
+    step = code_step_to_fixed(rate, fs)
+    nudge = int(round((step_chips % CODE_LENGTH) * CODE_SCALE))
+    return ((p0 + n * step + nudge) % CODE_MODULUS) / CODE_SCALE
+
+
+class _EplChan(C.Structure):
+    _fields_ = [("block_offset", C.c_int64), ("carrier_p0", C.c_uint64), ("carrier_step", C.c_uint64),
+                ("code_p0", C.c_uint64 * 3), ("code_step", C.c_uint64), ("prn", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class TrackEngine:
+    """Batched E/P/L correlators on one device (gacq_trk_*)."""
+
+    def __init__(self, device: int = 0):
+        self.device = int(device)
+        self._trk = C.c_void_p()
+        _lib.check(_lib.lib.gacq_trk_create(C.byref(self._trk), self.device))
+
+    def correlate(self, samples, offsets, states, config: TrackConfig) -> np.ndarray:
+        """E/P/L sums [C, 6] = (ie, qe, ip, qp, il, ql) for channel c over the block starting at
+        samples[offsets[c]] (complex64; host array, or CUDA array via __cuda_array_interface__)."""
+        states = list(states)
+        n = block_length(states[0], config)
+        for s in states:
+            if block_length(s, config) != n:
+                raise InvalidInputError("all channels of a batch need the same block length")
+        d = config.correlator_spacing_chips
+        chans = (_EplChan * len(states))()
+        for i, (st, off) in enumerate(zip(states, offsets)):
+            fs = st.sample_rate_hz
+            c = chans[i]
+            c.block_offset = int(off)
+            c.carrier_p0 = carrier_phase_to_fixed(st.carrier_phase_cycles)
+            c.carrier_step = carrier_step_to_fixed(st.doppler_hz, fs)
+            for j, o in enumerate((+d / 2, 0.0, -d / 2)):  # tracking.py:148-156
+                c.code_p0[j] = code_phase_to_fixed((st.code_phase_chips + o) % CODE_LENGTH)
+            c.code_step = code_step_to_fixed(st.code_rate_hz, fs)
+            c.prn = int(st.prn)
+        cai = getattr(samples, "__cuda_array_interface__", None)
+        flags = 0
+        if cai is not None:
+            if cai["typestr"] != "<c8":
+                raise InvalidInputError("device samples must be complex64")
+            total = int(np.prod(cai["shape"]))
+            ptr = cai["data"][0]
+            flags = _lib.SNAPS_ON_DEVICE
+        else:
+            arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
+            total, ptr = arr.size, arr.ctypes.data
+        out = np.empty((len(states), 6), dtype=np.float32)
+        _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, n, chans, len(states), flags, out.ctypes.data))
+        return out
+
+    def close(self):
+        if self._trk:
+            _lib.lib.gacq_trk_destroy(self._trk)
+            self._trk = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+_engines: dict = {}
+_lock = threading.Lock()
+
+
+def get_track_engine(device: int = 0) -> TrackEngine:
+    with _lock:
+        if device not in _engines:
+            _engines[device] = TrackEngine(device)
+        return _engines[device]
+
+
+def _outputs(sums: np.ndarray, n: int) -> list:
+    return [TrackOutput(ie=float(r[0]), qe=float(r[1]), ip=float(r[2]), qp=float(r[3]), il=float(r[4]),
+                        ql=float(r[5]), multiplications=4 * n, direct_equivalent_multiplications=n * n)
+            for r in sums]
+
+
+def epl_correlate(block, state: TrackState, config: TrackConfig, device: int = 0) -> TrackOutput:
+    """tracking.py:126-165 on the GPU."""
+    n = block_length(state, config)
+    samples = getattr(block, "samples", block)
+    if len(samples) != n:
+        raise InvalidInputError(f"block must hold {n} samples, got {len(samples)}")
+    return _outputs(get_track_engine(device).correlate(samples, [0], [state], config), n)[0]
+
+
+def _close_loops(out: TrackOutput, state: TrackState, config: TrackConfig):
+    """tracking.py:231-275 after the correlators: discriminators, loops, NCO advance, lock."""
+    ed = dll_discriminator(out, config.correlator_spacing_chips)
+    ep = pll_discriminator(out)
+    t = config.integration_ms * 1e-3
+    n = block_length(state, config)
+    g1p, _ = loop_gains(config.pll_bandwidth_hz)
+    g1d, _ = loop_gains(config.dll_bandwidth_hz)
+    _, pll_state = loop_filter(ep, state.pll_filter_state, config.pll_bandwidth_hz, t)
+    _, dll_state = loop_filter(ed, state.dll_filter_state, config.dll_bandwidth_hz, t)
+    doppler = state.doppler_hz + (pll_state[0] - state.pll_filter_state[0])
+    code_rate = CHIP_RATE_HZ * (1.0 + doppler / L1_CARRIER_HZ) + dll_state[0]
+    carrier_phase = _advance_carrier(state.carrier_phase_cycles, state.doppler_hz, state.sample_rate_hz, n,
+                                     t * g1p * ep)
+    code_phase = _advance_code(state.code_phase_chips, state.code_rate_hz, state.sample_rate_hz, n, t * g1d * ed)
+    nbd = out.ip * out.ip - out.qp * out.qp
+    nbp = out.ip * out.ip + out.qp * out.qp
+    if state.epoch == 0:
+        nbd_s, nbp_s = nbd, nbp
+    else:
+        alpha = 1.0 / LOCK_SMOOTHING_EPOCHS
+        nbd_s = state.lock_nbd + alpha * (nbd - state.lock_nbd)
+        nbp_s = state.lock_nbp + alpha * (nbp - state.lock_nbp)
+    lock = nbd_s / nbp_s if nbp_s > 0 else 0.0
+    new_state = replace(state, code_phase_chips=code_phase, carrier_phase_cycles=carrier_phase, doppler_hz=doppler,
+                        code_rate_hz=code_rate, dll_filter_state=dll_state, pll_filter_state=pll_state,
+                        epoch=state.epoch + 1, lock_nbd=nbd_s, lock_nbp=nbp_s)
+    return new_state, replace(out, dll_error_chips=ed, pll_error_cycles=ep, lock_metric=lock)
+
+
+def track_epoch(block, state: TrackState, config: TrackConfig, device: int = 0):
+    """tracking.py:226-275: one loop iteration (GPU correlators, host loop closure)."""
+    return _close_loops(epl_correlate(block, state, config, device), state, config)
+
+
+def track_epoch_batch(samples, offsets, states, config: TrackConfig, device: int = 0):
+    """One epoch for many channels in one device launch: channel c correlates
+    samples[offsets[c] : offsets[c] + N]. Returns (new_states, outputs), channel order kept."""
+    states = list(states)
+    if not states:
+        raise InvalidInputError("no channels")
+    n = block_length(states[0], config)
+    sums = get_track_engine(device).correlate(samples, offsets, states, config)
+    res = [_close_loops(o, s, config) for o, s in zip(_outputs(sums, n), states)]
+    return [r[0] for r in res], [r[1] for r in res]
