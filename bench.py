@@ -213,6 +213,62 @@ def synth_batch(torch, n, c, seed, device):
 
 
 # ------------------------------------------------------------------ arms
+def _cpu_track(arg):
+    """Oracle tracking (restated tracking.py:226-275) of a few channels of one snapshot."""
+    import oracle
+    from oracle import tracking_oracle as to
+
+    cname, x, prns, epochs = arg
+    c = CONFIGS[cname]
+    n = round(c["fs"] * 1e-3)
+    cfg = to.TrackConfig()
+    states = [to.init_from_acquisition(p, 0.0, 0, c["fs"]) for p in prns]
+    for k in range(epochs):
+        states = [to.track_epoch(x[k * n:(k + 1) * n], s, cfg)[0] for s in states]
+    return len(states) * epochs
+
+
+def measure_tracking(torch, dev, c, epochs, cpu, dist):
+    """every PRN of every snapshot in the batch tracked for `epochs`
+    1 ms epochs (one device launch for all channels per epoch + vectorised loop closure),
+    bit-exact with the reference's tracking (tests/test_gpu_tracking.py)."""
+    from paper_1309_0052_b200 import tracking as trk
+    from paper_1309_0052_b200.sharding import max_over_ranks
+
+    n_snap, span = dev.shape
+    n = round(c["fs"] * 1e-3)
+    epochs = max(1, min(epochs, span // n))
+    rng = np.random.default_rng(7)
+    prns = np.tile(np.arange(1, 33), n_snap)
+    states = [trk.TrackState(prn=int(p), code_phase_chips=float(rng.uniform(0, 1023)), carrier_phase_cycles=0.0,
+                             doppler_hz=float(d), code_rate_hz=1.023e6 * (1.0 + float(d) / 1575.42e6),
+                             sample_rate_hz=c["fs"]) for p, d in zip(prns, rng.uniform(-4750, 4750, prns.size))]
+    base = np.repeat(np.arange(n_snap, dtype=np.int64) * span, 32)
+    cfg = trk.TrackConfig()
+    batch0 = trk.TrackBatch.from_states(states)
+    trk.track_step(dev, base, batch0, cfg)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    batch = batch0
+    for k in range(epochs):
+        batch, outs = trk.track_step(dev, base + k * n, batch, cfg)
+    wall = max_over_ranks(time.perf_counter() - t0, dist, "cuda")
+    ws = dist.get_world_size() if dist else 1
+    res = {"metric": "tracking channel-epochs/s", "value": ws * prns.size * epochs / wall,
+           "unit": "channel-epochs/s", "channels_per_gpu": int(prns.size), "epochs": epochs,
+           "note": "one gacq_trk_epl launch (all channels) + vectorised float64 loop closure per epoch; "
+                   "device-resident samples; wall-clocked"}
+    if cpu:
+        import oracle
+
+        x = oracle.make_snapshot(0, c["fs"], c["rounds"] * 1e-3, base_seed=900)[0]
+        t0 = time.perf_counter()
+        m = _cpu_track((next(k for k, v in CONFIGS.items() if v is c), x, list(range(1, 9)), min(4, epochs)))
+        res["cpu_baseline"] = {"value": m / (time.perf_counter() - t0), "unit": "channel-epochs/s", "cores": 1,
+                               "kind": "port", "sample": f"{m} channel-epochs, oracle/tracking_oracle.py"}
+    return res
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -328,6 +384,9 @@ def run_ours(args, rank, world, local_rank):
                 "api": "AcqEngine.search_quantized(pinned int8 I/Q, GNSSIF01 payload)"}
     pinned8.close()
 
+    tracking = measure_tracking(torch, dev, c, args.steps if args.tracking_epochs <= 0 else args.tracking_epochs,
+                                rank == 0 and world == 1 and not args.no_cpu_baseline, dist)
+
     f_corr, f_fwd = flops_per_cell(c, n_bins)
     sm = props.multi_processor_count
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -371,6 +430,7 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": batch * 32 * 16, "api": "AcqEngine.search(pinned host batch)"},
         "e2e_int8": e2e_int8,
+        "tracking": tracking,
         "gpu_launches": st["launches"],
         "wall_ms_per_step": t_wall_max * 1e3 / args.steps,
         "clocks": clk.summary(),
@@ -393,6 +453,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="snapshots per GPU (default: config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tracking-epochs", type=int, default=10, help="tracking epochs measured (0: = --steps)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

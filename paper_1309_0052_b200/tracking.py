@@ -215,6 +215,22 @@ class TrackEngine:
         _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, n, chans, len(states), flags, out.ctypes.data))
         return out
 
+    def correlate_chans(self, samples, chans: np.ndarray, n: int) -> np.ndarray:
+        """Like correlate() but from prepared gacq_epl_chan records (tracking.EPL_CHAN_DTYPE)."""
+        chans = np.ascontiguousarray(chans)
+        cai = getattr(samples, "__cuda_array_interface__", None)
+        if cai is not None:
+            if cai["typestr"] != "<c8":
+                raise InvalidInputError("device samples must be complex64")
+            total, ptr, flags = int(np.prod(cai["shape"])), cai["data"][0], _lib.SNAPS_ON_DEVICE
+        else:
+            arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
+            total, ptr, flags = arr.size, arr.ctypes.data, 0
+        out = np.empty((chans.size, 6), dtype=np.float32)
+        _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, int(n), chans.ctypes.data, chans.size, flags,
+                                         out.ctypes.data))
+        return out
+
     def close(self):
         if self._trk:
             _lib.lib.gacq_trk_destroy(self._trk)
@@ -286,6 +302,140 @@ def _close_loops(out: TrackOutput, state: TrackState, config: TrackConfig):
 def track_epoch(block, state: TrackState, config: TrackConfig, device: int = 0):
     """tracking.py:226-275: one loop iteration (GPU correlators, host loop closure)."""
     return _close_loops(epl_correlate(block, state, config, device), state, config)
+
+
+# ---- struct-of-arrays batch path ------------------------------------------------------
+
+EPL_CHAN_DTYPE = np.dtype([("block_offset", "<i8"), ("carrier_p0", "<u8"), ("carrier_step", "<u8"),
+                           ("code_p0", "<u8", (3,)), ("code_step", "<u8"), ("prn", "<i4"), ("reserved", "<i4")])
+assert EPL_CHAN_DTYPE.itemsize == C.sizeof(_EplChan)
+
+
+def _carrier_phase_fixed_v(phase):  # kernels.py:56-58, vectorised (np.mod == Python %, rint == round)
+    return (np.rint(np.mod(phase, 1.0) * float(CARRIER_SCALE)).astype(np.int64) % CARRIER_SCALE).astype(np.uint64)
+
+
+def _carrier_step_fixed_v(freq, fs):  # kernels.py:61-62
+    return (np.rint((freq / fs) * float(CARRIER_SCALE)).astype(np.int64) % CARRIER_SCALE).astype(np.uint64)
+
+
+def _code_phase_fixed_v(phase):  # kernels.py:65-66
+    return (np.rint(np.mod(phase, 1023.0) * float(CODE_SCALE)).astype(np.int64) % CODE_MODULUS).astype(np.uint64)
+
+
+def _code_step_fixed_v(rate, fs):  # kernels.py:69-70
+    return np.rint((rate / fs) * float(CODE_SCALE)).astype(np.int64).astype(np.uint64)
+
+
+@dataclass
+class TrackBatch:
+    """TrackState fields as float64/int arrays over channels (struct of arrays)."""
+
+    prn: np.ndarray
+    code_phase_chips: np.ndarray
+    carrier_phase_cycles: np.ndarray
+    doppler_hz: np.ndarray
+    code_rate_hz: np.ndarray
+    dll_acc: np.ndarray
+    dll_prev: np.ndarray
+    pll_acc: np.ndarray
+    pll_prev: np.ndarray
+    epoch: np.ndarray
+    sample_rate_hz: np.ndarray
+    lock_nbd: np.ndarray
+    lock_nbp: np.ndarray
+
+    @classmethod
+    def from_states(cls, states) -> "TrackBatch":
+        s = list(states)
+        f = lambda k: np.array([getattr(x, k) for x in s], dtype=np.float64)  # noqa: E731
+        return cls(prn=np.array([x.prn for x in s], dtype=np.int32), code_phase_chips=f("code_phase_chips"),
+                   carrier_phase_cycles=f("carrier_phase_cycles"), doppler_hz=f("doppler_hz"),
+                   code_rate_hz=f("code_rate_hz"),
+                   dll_acc=np.array([x.dll_filter_state[0] for x in s], dtype=np.float64),
+                   dll_prev=np.array([x.dll_filter_state[1] for x in s], dtype=np.float64),
+                   pll_acc=np.array([x.pll_filter_state[0] for x in s], dtype=np.float64),
+                   pll_prev=np.array([x.pll_filter_state[1] for x in s], dtype=np.float64),
+                   epoch=np.array([x.epoch for x in s], dtype=np.int64), sample_rate_hz=f("sample_rate_hz"),
+                   lock_nbd=f("lock_nbd"), lock_nbp=f("lock_nbp"))
+
+    def to_states(self) -> list:
+        return [TrackState(prn=int(self.prn[i]), code_phase_chips=float(self.code_phase_chips[i]),
+                           carrier_phase_cycles=float(self.carrier_phase_cycles[i]), doppler_hz=float(self.doppler_hz[i]),
+                           code_rate_hz=float(self.code_rate_hz[i]),
+                           dll_filter_state=(float(self.dll_acc[i]), float(self.dll_prev[i])),
+                           pll_filter_state=(float(self.pll_acc[i]), float(self.pll_prev[i])), epoch=int(self.epoch[i]),
+                           sample_rate_hz=float(self.sample_rate_hz[i]), lock_nbd=float(self.lock_nbd[i]),
+                           lock_nbp=float(self.lock_nbp[i]))
+                for i in range(self.prn.size)]
+
+
+def epl_chans(batch: TrackBatch, offsets, config: TrackConfig) -> np.ndarray:
+    """gacq_epl_chan records for every channel of the batch (vectorised kernels.py:56-70)."""
+    d = config.correlator_spacing_chips
+    ch = np.zeros(batch.prn.size, dtype=EPL_CHAN_DTYPE)
+    ch["block_offset"] = np.asarray(offsets, dtype=np.int64)
+    ch["carrier_p0"] = _carrier_phase_fixed_v(batch.carrier_phase_cycles)
+    ch["carrier_step"] = _carrier_step_fixed_v(batch.doppler_hz, batch.sample_rate_hz)
+    for j, o in enumerate((+d / 2, 0.0, -d / 2)):  # tracking.py:148-156
+        ch["code_p0"][:, j] = _code_phase_fixed_v(np.mod(batch.code_phase_chips + o, float(CODE_LENGTH)))
+    ch["code_step"] = _code_step_fixed_v(batch.code_rate_hz, batch.sample_rate_hz)
+    ch["prn"] = batch.prn
+    return ch
+
+
+def close_loops_batch(sums: np.ndarray, batch: TrackBatch, config: TrackConfig):
+    """tracking.py:231-275 over a batch, in the reference's float64 operation order
+    (bit-identical per channel; atan via math.atan). Returns (new batch, outputs dict)."""
+    ie, qe, ip, qp, il, ql = (sums[:, i].astype(np.float64) for i in range(6))
+    e = ie * ie + qe * qe
+    l = il * il + ql * ql
+    dead = (e + l == 0) & (ip == 0) & (qp == 0)
+    if dead.any():
+        raise DegenerateInputError(f"all correlators zero on channel {int(np.flatnonzero(dead)[0])}")
+    sp = config.correlator_spacing_chips
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ed = np.where(e + l == 0, 0.0, (e - l) / (e + l) * (1.0 - sp / 2.0) / 2.0)
+        ratio = qp / ip
+    ep = np.array([math.copysign(0.25, q) if i == 0.0 else math.atan(r) / (2.0 * math.pi)
+                   for i, q, r in zip(ip.tolist(), qp.tolist(), ratio.tolist())], dtype=np.float64)
+    t = config.integration_ms * 1e-3
+    n = round(float(batch.sample_rate_hz[0]) * config.integration_ms * 1e-3)
+    g1p, g2p = loop_gains(config.pll_bandwidth_hz)
+    g1d, g2d = loop_gains(config.dll_bandwidth_hz)
+    pll_acc = batch.pll_acc + g2p * t * (ep + batch.pll_prev) / 2.0
+    dll_acc = batch.dll_acc + g2d * t * (ed + batch.dll_prev) / 2.0
+    doppler = batch.doppler_hz + (pll_acc - batch.pll_acc)
+    code_rate = CHIP_RATE_HZ * (1.0 + doppler / L1_CARRIER_HZ) + dll_acc
+    fs = batch.sample_rate_hz
+    pc = (_carrier_phase_fixed_v(batch.carrier_phase_cycles) + np.uint64(n) * _carrier_step_fixed_v(batch.doppler_hz, fs)
+          + _carrier_phase_fixed_v(t * g1p * ep)) % np.uint64(CARRIER_SCALE)
+    nudge = np.rint(np.mod(t * g1d * ed, float(CODE_LENGTH)) * float(CODE_SCALE)).astype(np.int64).astype(np.uint64)
+    pcode = (_code_phase_fixed_v(batch.code_phase_chips) + np.uint64(n) * _code_step_fixed_v(batch.code_rate_hz, fs)
+             + nudge) % np.uint64(CODE_MODULUS)
+    nbd = ip * ip - qp * qp
+    nbp = ip * ip + qp * qp
+    first = batch.epoch == 0
+    alpha = 1.0 / LOCK_SMOOTHING_EPOCHS
+    nbd_s = np.where(first, nbd, batch.lock_nbd + alpha * (nbd - batch.lock_nbd))
+    nbp_s = np.where(first, nbp, batch.lock_nbp + alpha * (nbp - batch.lock_nbp))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        lock = np.where(nbp_s > 0, nbd_s / nbp_s, 0.0)
+    new = TrackBatch(prn=batch.prn, code_phase_chips=pcode.astype(np.float64) / float(CODE_SCALE),
+                     carrier_phase_cycles=pc.astype(np.float64) / float(CARRIER_SCALE), doppler_hz=doppler,
+                     code_rate_hz=code_rate, dll_acc=dll_acc, dll_prev=ed, pll_acc=pll_acc, pll_prev=ep,
+                     epoch=batch.epoch + 1, sample_rate_hz=fs, lock_nbd=nbd_s, lock_nbp=nbp_s)
+    outs = dict(ie=ie, qe=qe, ip=ip, qp=qp, il=il, ql=ql, dll_error_chips=ed, pll_error_cycles=ep, lock_metric=lock)
+    return new, outs
+
+
+def track_step(samples, offsets, batch: TrackBatch, config: TrackConfig, device: int = 0):
+    """One epoch of a struct-of-arrays batch: one device launch + vectorised loop closure."""
+    eng = get_track_engine(device)
+    chans = epl_chans(batch, offsets, config)
+    n = round(float(batch.sample_rate_hz[0]) * config.integration_ms * 1e-3)
+    sums = eng.correlate_chans(samples, chans, n)
+    return close_loops_batch(sums, batch, config)
 
 
 def track_epoch_batch(samples, offsets, states, config: TrackConfig, device: int = 0):

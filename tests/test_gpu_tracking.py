@@ -106,6 +106,27 @@ def test_batch_epoch_equals_single_channel_epochs(trk):
     assert [o.ie for o in o_b] == [o.ie for o in o_c]
 
 
+def test_track_step_struct_of_arrays_bit_exact(trk):
+    """The batched path (one launch + vectorised closure per epoch, device-resident samples)
+    on the acquisition->tracking chain: every detected PRN of a C3 snapshot, 10 epochs."""
+    import torch
+
+    c = case("chain_c3_snap0")
+    bl = blocks(c)
+    cfg = trk.TrackConfig(**c["config"])
+    dev = torch.from_numpy(np.concatenate(bl)).cuda()
+    torch.cuda.synchronize()
+    n = bl[0].size
+    batch = trk.TrackBatch.from_states([to_state(trk, ch["init"]) for ch in c["channels"]])
+    for k in range(c["epochs"]):
+        batch, outs = trk.track_step(dev, [k * n] * batch.prn.size, batch, cfg)
+        for i, ch in enumerate(c["channels"]):
+            ref = ch["epochs"][k]
+            assert outs["ip"][i] == ref["ip"] and outs["ql"][i] == ref["ql"], (k, i)
+            assert batch.doppler_hz[i] == ref["state"]["doppler_hz"]
+            assert batch.code_phase_chips[i] == ref["state"]["code_phase_chips"]
+
+
 def test_tracking_api_semantics(trk):
     with pytest.raises(trk.InvalidConfigError):
         trk.TrackConfig(pll_bandwidth_hz=300.0)
