@@ -198,6 +198,21 @@ def test_c5_weak_signal_sweep_decisions(pkg, cn0):
     assert exact >= 4 * 32 - 1, (exact, ties)
 
 
+def test_acquire_batch_over_device_list(pkg):
+    """acquire_batch shards snapshots over `devices` (one host thread each); with the one
+    visible GPU listed twice the shards run concurrently on two plans of the same device."""
+    cs = [case(f"c3_snap{i}") for i in range(5)]
+    cfg = pkg.AcqConfig(**cs[0]["config"])
+    batch = np.stack([case_input(c) for c in cs])
+    got = pkg.acquire_batch(batch, cs[0]["fs"], list(range(1, 33)), cfg, devices=[0, 0])
+    assert len(got) == 5
+    for res, c in zip(got, cs):
+        for g, r in zip(res, c["results"]):
+            gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples,
+                      peak_metric=g.peak_metric, detected=g.detected)
+            assert compare(gd, r, c["config"]["detection_threshold"]) == "exact"
+
+
 def test_plans_with_different_rates_coexist(pkg):
     """Kernel attributes are process-wide: creating a D=2 plan after a D=4 one must not
     break the D=4 plan (regression: launch 'invalid argument')."""
