@@ -1,0 +1,41 @@
+"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck / synccheck):
+
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+
+Exercises every device kernel once: K1 (D=2, 4, 16), the persistent K2 (row in shared
+memory and in L2 scratch), K3, the int8 dequantizer and the tracking correlators.
+"""
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import oracle  # noqa: E402
+import paper_1309_0052_b200 as g  # noqa: E402
+from paper_1309_0052_b200 import tracking as trk  # noqa: E402
+
+
+def main():
+    for fs, rounds in ((2.046e6, 2), (4.092e6, 2), (16.368e6, 1)):
+        cfg = g.AcqConfig(doppler_min_hz=-1000.0, doppler_max_hz=1000.0, doppler_step_hz=500.0,
+                          noncoherent_rounds=rounds)
+        x = np.stack([oracle.make_snapshot(i, fs, rounds * 1e-3, base_seed=11)[0] for i in range(2)])
+        eng = g.AcqEngine(fs, [1, 5, 9], cfg)
+        r = eng.search(x)
+        q = np.clip(np.round(np.stack([x.real, x.imag], -1).reshape(2, -1) / 40.0 * 127), -127, 127).astype(np.int8)
+        eng.search_quantized(q, 0, 40.0)
+        eng.close()
+        print(fs, r.code_phase_samples[0].tolist())
+    st = [trk.TrackState(prn=p, code_phase_chips=10.0 * p, carrier_phase_cycles=0.0, doppler_hz=100.0 * p,
+                         code_rate_hz=1.023e6, sample_rate_hz=4.092e6) for p in (1, 2, 3)]
+    blk = oracle.make_snapshot(0, 4.092e6, 1e-3, base_seed=3)[0]
+    s2, out = trk.track_epoch_batch(blk, [0, 0, 0], st, trk.TrackConfig())
+    print("track", [round(o.ip, 2) for o in out])
+
+
+if __name__ == "__main__":
+    main()
