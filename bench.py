@@ -310,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
     cfg = g.AcqConfig(**acq_kwargs(c))
     n_bins = cfg.doppler_bins_hz().size
     batch = args.batch or c["batch"]
-    eng = g.AcqEngine(c["fs"], list(range(1, 33)), cfg, device=local_rank)
+    eng = g.AcqEngine(c["fs"], list(range(1, 33)), cfg, device=local_rank, scratch_bytes=args.scratch_mb << 20)
     dev = synth_batch(torch, batch, c, seed=1000 + rank, device=torch.device("cuda", local_rank))
     pinned = g.PinnedBuffer(tuple(dev.shape))
     pinned.array[...] = dev.cpu().numpy()
@@ -454,6 +454,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tracking-epochs", type=int, default=10, help="tracking epochs measured (0: = --steps)")
+    ap.add_argument("--scratch-mb", type=int, default=0, help="spectrum scratch (MiB, both halves); 0 = library default")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
