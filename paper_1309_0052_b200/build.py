@@ -15,8 +15,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB = PKG / "libgacq.so"
 SOURCES = [PKG / "csrc" / "gacq.cu"]
-DEPS = SOURCES + [PKG / "csrc" / "gacq_kernels.cuh", PKG / "csrc" / "codelets.cuh", PKG / "csrc" / "gtrk_kernels.cuh",
-                  ROOT / "include" / "gacq.h"]
+DEPS = SOURCES + [PKG / "csrc" / h for h in ("gacq_kernels.cuh", "gacq_pfa.cuh", "pfa.cuh", "pfa_tables.cuh",
+                                             "codelets.cuh", "gtrk_kernels.cuh")] + [ROOT / "include" / "gacq.h"]
 
 
 def nvcc() -> str:

@@ -15,6 +15,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -22,6 +23,7 @@
 #include <vector>
 
 #include "gacq_kernels.cuh"
+#include "gacq_pfa.cuh"
 #include "gtrk_kernels.cuh"
 
 using namespace gacq;
@@ -116,7 +118,10 @@ struct gacq_ctx {
     int device = 0;
     double fs = 0;
     int n_coh = 0, P = 0, D = 0, K = 0, R = 0, B = 0, n_prn = 0, radius = 0;
-    int ng = 1;  // K1 transform groups per CTA
+    int ng = 1;  // K1 transform groups per CTA (2048-point path)
+    bool pfa = true;  // 1023-point prime-factor path (gacq_pfa.cuh); GACQ_PATH=2048 selects the other
+    int cw = 4, cpw = 1;  // PFA K2: warps per CTA, phases per warp
+    float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kBuf]
     std::vector<double> bins;
     std::vector<int32_t> prns;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -194,6 +199,40 @@ bool fwd_supported(int D) {
     GACQ_FWD_VARIANTS(GACQ_HAS_FWD)
 #undef GACQ_HAS_FWD
     return false;
+}
+
+// PFA K1 instantiations: (D, warps per CTA)
+#define GACQ_PFA_FWD_VARIANTS(X) X(1, 1) X(2, 2) X(4, 4) X(5, 5) X(6, 6) X(8, 8) X(13, 7) X(14, 7) X(16, 8)
+
+cudaError_t launch_fwd_pfa(const gacq_ctx* c, const FwdPfaArgs& fa, int64_t blocks) {
+#define GACQ_LAUNCH_FWDP(DD, WW)                                                                        \
+    if (c->D == DD) {                                                                                   \
+        gacq_fwd_pfa_kernel<DD, WW><<<(unsigned)blocks, 32 * WW, fwd_pfa_smem(DD, WW), c->stream>>>(fa); \
+        return cudaGetLastError();                                                                      \
+    }
+    GACQ_PFA_FWD_VARIANTS(GACQ_LAUNCH_FWDP)
+#undef GACQ_LAUNCH_FWDP
+    return cudaErrorInvalidConfiguration;
+}
+
+// K2 shape: PW phases per warp, W = ceil(D/PW) <= 6 warps; among the two smallest feasible
+// PW take the one with the least idle phase slots (W PW - D), ties -> more warps.
+void corr_pfa_shape(int D, int* W, int* PW) {
+    const int p0 = (D + kCorrMaxWarps - 1) / kCorrMaxWarps;
+    int best_pw = p0, best_w = (D + p0 - 1) / p0;
+    const int w1 = (D + p0) / (p0 + 1);
+    if (w1 * (p0 + 1) < best_w * best_pw) { best_pw = p0 + 1; best_w = w1; }
+    *W = best_w;
+    *PW = best_pw;
+}
+
+cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
+    const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
+    if (c->cpw == 1)
+        gacq_corr_pfa_kernel<true><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
+    else
+        gacq_corr_pfa_kernel<false><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_corr(const gacq_ctx* c, const CorrArgs& ca) {
@@ -313,15 +352,27 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
                 CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[k], 0));
             waited = std::max(waited, need);
         }
-        FwdArgs fa{in, in_stride, c->d_carrier, c->d_tw, c->d_Z, p0, c->B, c->R, c->n_coh, c->P, c->D, c->K};
+        cx* Zp = reinterpret_cast<cx*>(c->d_Z);
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
-        CUDA_TRY(launch_fwd(c, fa, np * c->R));
+        if (c->pfa) {
+            FwdPfaArgs fa{in, in_stride, c->d_carrier, Zp, p0, c->B, c->R, c->n_coh, c->P, c->K};
+            CUDA_TRY(launch_fwd_pfa(c, fa, np * c->R));
+        } else {
+            FwdArgs fa{in, in_stride, c->d_carrier, c->d_tw, c->d_Z, p0, c->B, c->R, c->n_coh, c->P, c->D, c->K};
+            CUDA_TRY(launch_fwd(c, fa, np * c->R));
+        }
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
         CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
-        CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, np * c->n_prn,
-                    c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius};
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
-        CUDA_TRY(launch_corr(c, ca));
+        if (c->pfa) {
+            CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
+                           np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw};
+            CUDA_TRY(launch_corr_pfa(c, ca));
+        } else {
+            CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, np * c->n_prn,
+                        c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius};
+            CUDA_TRY(launch_corr(c, ca));
+        }
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
         c->stats.fwd_launches++;
         c->stats.corr_launches++;
@@ -376,6 +427,7 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_cc);
         cudaFree(c->d_tw);
         cudaFree(c->d_Z);
+        cudaFree(c->d_ccp);
         cudaFree(c->d_in);
         cudaFree(c->d_raw);
         cudaFree(c->d_rows_bin);
@@ -463,6 +515,8 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->n_prn = p->n_prn;
     c->radius = p->exclusion_radius_samples ? p->exclusion_radius_samples : (int)std::ceil(fs / kChipRate);
     c->ng = D >= 2 ? 2 : 1;
+    if (const char* ev = std::getenv("GACQ_PATH")) c->pfa = std::strcmp(ev, "2048") != 0;
+    corr_pfa_shape(D, &c->cw, &c->cpw);
     c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
     c->prns.assign(p->prns, p->prns + p->n_prn);
 
@@ -502,6 +556,36 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     }
     std::vector<float2> tw(kM);
     for (int e = 0; e < kM; ++e) tw[e] = make_float2((float)std::cos(kTwoPi * e / kM), (float)std::sin(kTwoPi * e / kM));
+    // PFA path: conj(DFT_1023(chip)) / 1023 in float64, spectrum index k = (528 k1 + 496 k2)
+    // mod 1023 stored at [k2][k1] (gacq_pfa.cuh); column 31 of each row is zero padding
+    std::vector<float2> ccp((size_t)c->n_prn * kBuf, make_float2(0.f, 0.f));
+    {
+        std::vector<double> cs(kChips), sn(kChips);
+        for (int m = 0; m < kChips; ++m) {
+            cs[m] = std::cos(kTwoPi * m / kChips);
+            sn[m] = std::sin(kTwoPi * m / kChips);
+        }
+        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 16));
+        std::vector<std::thread> th;
+        for (int w = 0; w < nt; ++w)
+            th.emplace_back([&, w]() {
+                for (int i = w; i < c->n_prn; i += nt) {
+                    int8_t chips[kChips];
+                    ca_code(c->prns[i], chips);
+                    for (int k = 0; k < kChips; ++k) {
+                        double re = 0, im = 0;
+                        for (int j = 0, m = 0; j < kChips; ++j, m = m + k >= kChips ? m + k - kChips : m + k) {
+                            re += chips[j] * cs[m];
+                            im -= chips[j] * sn[m];
+                        }
+                        // conj / 1023
+                        ccp[(size_t)i * kBuf + (k % 33) * 32 + k % 31] =
+                            make_float2((float)(re / kChips), (float)(-im / kChips));
+                    }
+                }
+            });
+        for (auto& t : th) t.join();
+    }
 
     // ---- device state ---------------------------------------------------------------
     DeviceGuard guard(c->device);
@@ -522,10 +606,38 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     CTX_TRY(cudaMemcpy(c->d_carrier, carrier.data(), carrier.size() * sizeof(float2), cudaMemcpyHostToDevice));
     CTX_TRY(cudaMemcpy(c->d_cc, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice));
     CTX_TRY(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    const int64_t pair_bytes = (int64_t)c->R * c->D * kM * (int64_t)sizeof(float2);
+    CTX_TRY(cudaMalloc(&c->d_ccp, ccp.size() * sizeof(float2)));
+    CTX_TRY(cudaMemcpy(c->d_ccp, ccp.data(), ccp.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    const int64_t pair_bytes = (int64_t)c->R * c->D * (c->pfa ? kBuf : kM) * (int64_t)sizeof(float2);
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
+    if (c->pfa) {
+        // every PFA variant gets the largest dynamic shared memory any plan launches it with
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     corr_pfa_smem(kCorrMaxWarps)));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     corr_pfa_smem(kCorrMaxWarps)));
+#define GACQ_ATTR_FWDP(DD, WW)                                                                             \
+    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_pfa_kernel<DD, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 fwd_pfa_smem(DD, WW)));
+        GACQ_PFA_FWD_VARIANTS(GACQ_ATTR_FWDP)
+#undef GACQ_ATTR_FWDP
+        int per_sm = 0, sms = 0;
+        if (c->cpw == 1)
+            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<true>, 32 * c->cw,
+                                                                  corr_pfa_smem(c->cw)));
+        else
+            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<false>, 32 * c->cw,
+                                                                  corr_pfa_smem(c->cw)));
+        CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+        c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
+        if (c->cpw > 1)
+            CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kChips * sizeof(float)));
+        CTX_TRY(cudaMalloc(&c->d_counter, sizeof(unsigned long long)));
+        *out = c;
+        return GACQ_OK;
+    }
     // Function attributes are process-wide (shared by every plan), so each kernel gets the
     // largest dynamic shared memory any plan can launch it with -- a function of its
     // template parameters only, never of this plan.
@@ -562,11 +674,11 @@ int gacq_info_get(const gacq_ctx* c, gacq_info* o) {
     o->samples_per_period = c->P;
     o->n_coh = c->n_coh;
     o->chip_oversample = c->D;
-    o->fft_len = kM;
+    o->fft_len = c->pfa ? kChips : kM;
     o->n_bins = c->B;
     o->n_prn = c->n_prn;
     o->rounds = c->R;
-    o->path = 1;
+    o->path = c->pfa ? 2 : 1;
     return GACQ_OK;
 }
 

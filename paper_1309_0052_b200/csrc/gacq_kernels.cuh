@@ -146,36 +146,27 @@ struct FwdArgs {
 // both the wipe stores (consecutive n) and the chip-sum loads (consecutive m) conflict-free.
 __host__ __device__ constexpr int fwd_ws(int D) { return kRow + (D <= 16 ? 16 / D : 0); }
 
-// grid: (pairs_in_chunk * R) blocks of NG*128 threads;
-// dynamic smem: (D*fwd_ws(D) + NG*2*kXchg) cx
-template <int NG, int D>
-__global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
+// Wipe-off (bit-exact, acquisition.py:141) of one coherent block x (K code periods) with the
+// carrier replica c, folded over the K periods into the transposed table
+// wt[k][m] = wbar[D m + k]; wt[k][1023] repeats wt[k][0] (circular chip m+1). Coalesced,
+// two samples per 16-byte load. All NT threads of the CTA take part; ends with a barrier.
+template <int D, int NT>
+__device__ __forceinline__ void wipe_fold(const cx* __restrict__ x, const cx* __restrict__ c, int P, int K,
+                                          cx* __restrict__ wt) {
     constexpr int WS = fwd_ws(D);
-    extern __shared__ cx smem[];
-    cx* wt = smem;
-    const int lp = blockIdx.x / a.R, rd = blockIdx.x % a.R;
-    const int64_t pair = a.pair0 + lp;
-    const int64_t s = pair / a.B;
-    const int b = (int)(pair % a.B);
-    const cx* x = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh;
-    const cx* c = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
-
-    // (A) wipe-off (bit-exact, acquisition.py:141) folded over the K code periods, coalesced
-    //     two samples per 16-byte load; wt[k][1023] repeats wt[k][0] (circular chip m+1).
-    constexpr int NT = NG * kT;
     auto put = [&](int n, cx w) {
         const int m = n / D, k = n - m * D;
         wt[k * WS + m] = w;
         if (m == 0) wt[k * WS + kChips] = w;
     };
-    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0 && (a.P & 1) == 0;
+    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0 && (P & 1) == 0;
     if (vec) {
         const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x);
         const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(c);
-        const int np = a.P / 2;
+        const int np = P / 2;
         for (int base = threadIdx.x; base < np; base += 4 * NT) {
             cx w[4][2];
-            for (int k = 0; k < a.K; ++k) {
+            for (int k = 0; k < K; ++k) {
                 ulonglong2 xv[4], cv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -202,13 +193,30 @@ __global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
             }
         }
     } else {
-        for (int n = threadIdx.x; n < a.P; n += NT) {
+        for (int n = threadIdx.x; n < P; n += NT) {
             cx acc = cmul_exact(__ldg(&x[n]), __ldg(&c[n]));
-            for (int k = 1; k < a.K; ++k) acc = add2(acc, cmul_exact(__ldg(&x[k * a.P + n]), __ldg(&c[k * a.P + n])));
+            for (int k = 1; k < K; ++k) acc = add2(acc, cmul_exact(__ldg(&x[k * P + n]), __ldg(&c[k * P + n])));
             put(n, acc);
         }
     }
     __syncthreads();
+}
+
+// grid: (pairs_in_chunk * R) blocks of NG*128 threads;
+// dynamic smem: (D*fwd_ws(D) + NG*2*kXchg) cx
+template <int NG, int D>
+__global__ void __launch_bounds__(NG * kT) gacq_fwd_kernel(FwdArgs a) {
+    constexpr int WS = fwd_ws(D);
+    extern __shared__ cx smem[];
+    cx* wt = smem;
+    const int lp = blockIdx.x / a.R, rd = blockIdx.x % a.R;
+    const int64_t pair = a.pair0 + lp;
+    const int64_t s = pair / a.B;
+    const int b = (int)(pair % a.B);
+    const cx* x = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh;
+    const cx* c = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
+    // (A) wipe-off + fold
+    wipe_fold<D, NG * kT>(x, c, a.P, a.K, wt);
 
     // (B) group g transforms phases g, g+NG, ...; thread t owns chips m = t + 128 r (r < 8),
     //     exactly its pass-0 inputs: z_rho[m] = sum_{i<D} wbar[D m + rho + i], computed

@@ -1,0 +1,342 @@
+// gacq_pfa.cuh -- K1/K2 of the acquisition hot path on the 1023-point prime-factor transform.
+//
+// Reference path: gnssperf/acquisition.py:128-159 (hot loop 138-149).
+//
+// The chip-polyphase reduction is the one of gacq_kernels.cuh: lag tau = D q + rho of the
+// reference's circular correlation over P = 1023 D samples equals the 1023-chip circular
+// correlation of z_rho[m] = sum_{i<D} wbar[(D m + rho + i) mod P] with the chips. Here that
+// correlation is evaluated with no zero padding:
+//   g_rho = IDFT_1023( DFT_1023(z_rho) * Cc ),  Cc = conj(DFT_1023(chip)) / 1023,
+// using the 31 x 33 Good-Thomas transform of pfa.cuh (no twiddles), one warp per transform:
+//   K1 forward:  31-point stage over n1 (lane = n2, row 32 spread over the warp), exchange,
+//                33-point stage over n2 (lane = k1 < 31), spectrum stored as Z[k2][32 lanes].
+//   K2 inverse:  Z * Cc on load, 33-point stage over k2 (lane = k1 < 31), exchange in place,
+//                31-point stage over k1 (lane = q2, row 32 spread), |.|^2 accumulated over rounds
+//                in registers for the cells (q1, q2), q = (33 q1 + 31 q2) mod 1023.
+// The spectrum of a transform is 33 x 32 complex64 = 8448 B; K2 streams each one into shared
+// memory with a bulk async copy (cp.async.bulk + mbarrier), double-buffered per warp.
+#pragma once
+#include "gacq_kernels.cuh"
+#include "pfa.cuh"
+
+namespace gacq {
+
+constexpr int kBuf = 33 * 32;                    // spectrum [k2][32]; column 31 is padding
+constexpr int kScr = 34;                         // coop31 scratch (33 used; keeps 16 B alignment)
+constexpr unsigned kSpecBytes = kBuf * sizeof(cx);
+constexpr int kCorrMaxWarps = 6;
+constexpr int kCorrWarpCx = 2 * kBuf + kScr;     // per-warp shared memory (cx)
+#ifndef GACQ_PFA_MAXNREG
+#define GACQ_PFA_MAXNREG 208                     // no spills; 168 would give 12 warps/SM with spills
+#endif
+
+__host__ __device__ constexpr int corr_pfa_smem(int W) { return W * (kCorrWarpCx * 8 + 16); }
+__host__ __device__ constexpr int fwd_pfa_smem(int D, int W) { return 8 * (D * fwd_ws(D) + W * (kBuf + kScr)); }
+
+// ---- bulk async copy + mbarrier (SASS UBLKCP / SYNCS) ------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// `bytes` from global `src` into shared `dst`; completion is signalled on `bar`. Issued by one
+// lane after the warp's generic accesses of `dst` (ordered by a __syncwarp before the call).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ float pow_acc(cx v, float acc) { return fmaf(im(v), im(v), fmaf(re(v), re(v), acc)); }
+
+// ---- K1 ---------------------------------------------------------------------------------
+struct FwdPfaArgs {
+    const float2* snaps;   // batch base (device), snapshot s at snaps + s*stride
+    int64_t stride;        // complex samples between snapshots
+    const float2* carrier; // [B][n_coh] wipe-off replicas
+    cx* Z;                 // [pairs][R][D][kBuf] spectra
+    int64_t pair0;         // first (snapshot, bin) pair of this chunk, pair = s*B + b
+    int B, R, n_coh, P, K;
+};
+
+// grid: pairs_in_chunk * R CTAs (one per (pair, round)) of 32 W threads. Warp w transforms
+// phases rho in [w PWF, (w+1) PWF), PWF = ceil(D/W), sliding the chip sums by one sample per
+// phase. dynamic smem: fwd_pfa_smem(D, W).
+template <int D, int W>
+__global__ void __launch_bounds__(32 * W) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
+    constexpr int WS = fwd_ws(D);
+    constexpr int PWF = (D + W - 1) / W;
+    extern __shared__ __align__(16) cx smem[];
+    cx* wt = smem;
+    const int lp = blockIdx.x / a.R, rd = blockIdx.x % a.R;
+    const int64_t pair = a.pair0 + lp;
+    const int64_t s = pair / a.B;
+    const int b = (int)(pair % a.B);
+    wipe_fold<D, 32 * W>(reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh,
+                         reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh, a.P, a.K, wt);
+
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cx* T = smem + D * WS + w * (kBuf + kScr);  // exchange [k1][33]
+    cx* scr = T + kBuf;
+    float coef[15];
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) coef[j - 1] = coop31_coef(lane, j);
+    // lane n2 holds z at m = (33 n1 + 31 n2) mod 1023, n1 < 31; lane L < 31 also holds row
+    // n2 = 32 at m = (33 L + 992) mod 1023
+    const int mb = 31 * lane, me = (33 * lane + 992) % kChips;
+    auto chip_sum = [&](int rho, int m) {
+        cx acc = czero();
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int k = rho + i;
+            acc = add2(acc, k < D ? wt[k * WS + m] : wt[(k - D) * WS + m + 1]);
+        }
+        return acc;
+    };
+    cx zr[31], ze;
+    const int rho0 = w * PWF;
+#pragma unroll 1
+    for (int ph = 0; ph < PWF; ++ph) {
+        const int rho = rho0 + ph;
+        if (rho >= D) break;
+        if (ph == 0) {
+#pragma unroll
+            for (int n1 = 0; n1 < 31; ++n1) {
+                int m = mb + 33 * n1;
+                m -= m >= kChips ? kChips : 0;
+                zr[n1] = chip_sum(rho, m);
+            }
+            ze = lane < 31 ? chip_sum(rho, me) : czero();
+        } else {  // window [rho-1, rho-1+D) -> [rho, rho+D): drop wbar[D m + rho-1], add wbar[D (m+1) + rho-1]
+            const cx* r = wt + (rho - 1) * WS;
+#pragma unroll
+            for (int n1 = 0; n1 < 31; ++n1) {
+                int m = mb + 33 * n1;
+                m -= m >= kChips ? kChips : 0;
+                zr[n1] = add2(sub2(zr[n1], r[m]), r[m + 1]);
+            }
+            if (lane < 31) ze = add2(sub2(ze, r[me]), r[me + 1]);
+        }
+        // 31-point stage over n1 -> T[k1][n2]
+        {
+            cx x[31];
+#pragma unroll
+            for (int n1 = 0; n1 < 31; ++n1) x[n1] = zr[n1];
+            dft_odd<-1, 31, 5>(x, [&](int k1, cx v) { T[k1 * 33 + lane] = v; });
+            coop31<-1>(ze, lane, [&](int j) { return coef[j - 1]; }, scr,
+                       [&](int, int k1, cx v) { T[k1 * 33 + 32] = v; });
+        }
+        __syncwarp();
+        // 33-point stage over n2 -> Z[k2][k1], coalesced 256 B stores
+        if (lane < 31) {
+            cx y[33];
+#pragma unroll
+            for (int n2 = 0; n2 < 33; ++n2) y[n2] = T[lane * 33 + n2];
+            cx* dst = a.Z + (((int64_t)lp * a.R + rd) * D + rho) * kBuf + lane;
+            dft33<-1>(y, [&](int k2, cx v) { dst[k2 * 32] = v; });
+        }
+        __syncwarp();
+    }
+}
+
+// ---- K2 ---------------------------------------------------------------------------------
+struct CorrPfaArgs {
+    const cx* Z;           // spectra of this chunk, [pairs][R][D][kBuf]
+    const cx* Cc;          // [n_prn][kBuf] conj code spectra / 1023, layout [k2][32]
+    gacq_row* rows_bin;    // [n_snap][n_prn][B]
+    float* pmap;           // optional [n_prn][B][P] power map (single snapshot), else null
+    float* row_scratch;    // [gridDim][D][1023] native-order power rows when PW > 1
+    int64_t pair0;
+    int64_t n_items;       // pairs_in_chunk * n_prn, item = lp * n_prn + pi
+    unsigned long long* counter;  // zeroed before the launch
+    int B, R, D, P, n_prn, radius, PW;
+};
+
+// chip lag of cell (q1, q2)
+__device__ __forceinline__ int cell_q(int q1, int q2) {
+    const int q = 33 * q1 + 31 * q2;
+    return q >= 2 * kChips ? q - 2 * kChips : q >= kChips ? q - kChips : q;
+}
+__device__ __forceinline__ bool better(float v, int l, float bv, int bl) { return v > bv || (v == bv && l < bl); }
+__device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
+    int d = abs(lag - peak);
+    d = min(d, P - d);
+    return d <= radius;
+}
+
+// Persistent: gridDim.x = resident CTA slots of 32 W threads; CTA c starts with item c and
+// claims the following items in order from a global counter, so the CTAs sharing a pair's
+// spectra run together and hit them in L2. Warp w owns phases [w PW, w PW + PW) of the item.
+// kRegs (PW == 1): the powers stay in registers through the argmax and the floor.
+// dynamic smem: corr_pfa_smem(W).
+template <bool kRegs>
+__global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
+    __shared__ float red_v[kCorrMaxWarps], red_f[kCorrMaxWarps];
+    __shared__ int red_i[kCorrMaxWarps];
+    __shared__ long long s_next;
+    __shared__ float s_coef[15][32];  // coop31 columns, read conflict-free as s_coef[j-1][lane]
+    extern __shared__ __align__(16) cx smem[];
+    const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 15 * 32; i += blockDim.x) s_coef[i >> 5][i & 31] = coop31_coef(i & 31, (i >> 5) + 1);
+    __syncthreads();
+    cx* buf = smem + w * kCorrWarpCx;  // buf[0..kBuf), buf[kBuf..2kBuf)
+    cx* scr = buf + 2 * kBuf;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + W * kCorrWarpCx) + 2 * w;
+    if (lane == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    const int rho0 = w * a.PW;
+    const int n_tr = min(a.PW, a.D - rho0) * a.R;  // transforms of this warp per item
+    auto src = [&](int64_t item, int j) {
+        const int64_t lp = item / a.n_prn;
+        return a.Z + ((lp * a.R + j % a.R) * a.D + rho0 + j / a.R) * kBuf;
+    };
+    int64_t item = blockIdx.x;
+    if (item >= a.n_items) return;
+    unsigned t = 0;  // this warp's transform count: buffer t & 1, mbarrier parity (t >> 1) & 1
+    if (lane == 0) bulk_load(buf, src(item, 0), kSpecBytes, &mbar[0]);
+    float* rows = a.row_scratch + (int64_t)blockIdx.x * a.D * kChips;
+
+    for (;;) {
+        if (threadIdx.x == 0) s_next = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
+        __syncthreads();
+        const int64_t next = s_next;
+        const int64_t lp = item / a.n_prn;
+        const int pi = (int)(item % a.n_prn);
+        const cx* cc = a.Cc + (int64_t)pi * kBuf + lane;
+
+        float best = -1.f;
+        int bidx = 0x7fffffff;
+        float acc[31], accx[2];
+#pragma unroll 1
+        for (int j = 0; j < n_tr; ++j, ++t) {
+            if (j % a.R == 0) {
+#pragma unroll
+                for (int i = 0; i < 31; ++i) acc[i] = 0.f;
+                accx[0] = accx[1] = 0.f;
+            }
+            if (lane == 0) {  // prefetch the warp's next spectrum into the other buffer
+                const cx* nsrc = j + 1 < n_tr ? src(item, j + 1) : next < a.n_items ? src(next, 0) : nullptr;
+                if (nsrc) bulk_load(buf + ((t + 1) & 1) * kBuf, nsrc, kSpecBytes, &mbar[(t + 1) & 1]);
+            }
+            mbar_wait(&mbar[t & 1], (t >> 1) & 1);
+            cx* E = buf + (t & 1) * kBuf;
+            // Z * Cc and the 33-point stage over k2; results E[q2][k1] written in place
+            cx x[33];
+            if (lane < 31) {
+#pragma unroll
+                for (int k2 = 0; k2 < 33; ++k2) x[k2] = cmul(E[k2 * 32 + lane], __ldg(cc + k2 * 32));
+            }
+            __syncwarp();
+            if (lane < 31) dft33<1>(x, [&](int q2, cx v) { E[q2 * 31 + lane] = v; });
+            __syncwarp();
+            // 31-point stage over k1 for row q2 = lane (+ row 32 spread over the warp)
+            const cx e = lane < 31 ? E[32 * 31 + lane] : czero();
+            const cx* Er = E + lane * 31;
+            dft31_stream<1>([&](int k1) { return Er[k1]; }, [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+            coop31<1>(e, lane, [&](int j) { return s_coef[j - 1][lane]; }, scr,
+                      [&](int sl, int, cx v) { accx[sl] = pow_acc(v, accx[sl]); });
+            __syncwarp();  // E is free for the prefetch issued at the next transform
+
+            if (!kRegs && j % a.R == a.R - 1) {  // phase done: spill to the row, track the argmax
+                const int rho = rho0 + j / a.R;
+                float* row = rows + rho * kChips;
+#pragma unroll
+                for (int q1 = 0; q1 < 31; ++q1) {
+                    row[q1 * 33 + lane] = acc[q1];
+                    const int lag = a.D * cell_q(q1, lane) + rho;
+                    if (better(acc[q1], lag, best, bidx)) { best = acc[q1]; bidx = lag; }
+                }
+                if (lane >= 1 && lane <= 16) {
+#pragma unroll
+                    for (int sl = 0; sl < 2; ++sl) {
+                        if (lane == 16 && sl == 1) break;
+                        const int q1 = lane == 16 ? 0 : sl ? 31 - lane : lane;
+                        row[q1 * 33 + 32] = accx[sl];
+                        const int lag = a.D * cell_q(q1, 32) + rho;
+                        if (better(accx[sl], lag, best, bidx)) { best = accx[sl]; bidx = lag; }
+                    }
+                }
+            }
+        }
+        // cells of this lane (kRegs): (q1, lane) for q1 < 31, and coop cells
+        auto for_cells = [&](auto&& f) {
+#pragma unroll
+            for (int q1 = 0; q1 < 31; ++q1) f(acc[q1], a.D * cell_q(q1, lane) + rho0);
+            if (lane >= 1 && lane <= 15) {
+                f(accx[0], a.D * cell_q(lane, 32) + rho0);
+                f(accx[1], a.D * cell_q(31 - lane, 32) + rho0);
+            } else if (lane == 16) {
+                f(accx[0], a.D * cell_q(0, 32) + rho0);
+            }
+        };
+        if (kRegs) for_cells([&](float v, int lag) { if (better(v, lag, best, bidx)) { best = v; bidx = lag; } });
+        // first argmax of the item (acquisition.py:151): ties -> lowest lag
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+            if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
+        }
+        if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
+        __syncthreads();  // (also publishes the row spills of every warp)
+        best = red_v[0];
+        bidx = red_i[0];
+        for (int i = 1; i < W; ++i)
+            if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
+        const int peak = bidx;
+        // exclusion floor (acquisition.py:155-159)
+        const int64_t pair = a.pair0 + lp;
+        const int64_t s = pair / a.B;
+        const int b = (int)(pair % a.B);
+        float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
+        float fl = -1.f;
+        if (kRegs) {
+            for_cells([&](float v, int lag) {
+                if (!excluded(lag, peak, a.P, a.radius)) fl = fmaxf(fl, v);
+                if (pm) pm[lag] = v;
+            });
+        } else {
+            for (int i = threadIdx.x; i < a.D * kChips; i += blockDim.x) {
+                const int rho = i / kChips, r = i - rho * kChips, q1 = r / 33, q2 = r - q1 * 33;
+                const int lag = a.D * cell_q(q1, q2) + rho;
+                const float v = rows[i];
+                if (!excluded(lag, peak, a.P, a.radius)) fl = fmaxf(fl, v);
+                if (pm) pm[lag] = v;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
+        if (lane == 0) red_f[w] = fl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float f = red_f[0];
+            for (int i = 1; i < W; ++i) f = fmaxf(f, red_f[i]);
+            gacq_row out;
+            out.bin = b;
+            out.lag = peak;
+            out.peak = best;
+            out.floor = f < 0.f ? 0.f : f;
+            a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
+        }
+        item = next;
+        if (item >= a.n_items) break;
+    }
+}
+
+}  // namespace gacq
