@@ -59,6 +59,8 @@ __device__ __forceinline__ cx rot(cx a) {
 }
 // a * w (general complex product: 2 instructions)
 __device__ __forceinline__ cx cmul(cx a, cx w) { return fma2(rot<1>(a), bc(im(w)), mul2(a, bc(re(w)))); }
+// a * conj(w)
+__device__ __forceinline__ cx cmul_conj(cx a, cx w) { return fma2(rot<1>(a), bc(-im(w)), mul2(a, bc(re(w)))); }
 __device__ __forceinline__ float cmag2(cx a) { return re(a) * re(a) + im(a) * im(a); }
 
 // exact complex64 product of kernels.py:78-86: round(round(ar*br) - round(ai*bi)),

@@ -366,7 +366,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
         if (c->pfa) {
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
-                           np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw};
+                           np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw, 0};
             CUDA_TRY(launch_corr_pfa(c, ca));
         } else {
             CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, np * c->n_prn,
@@ -558,7 +558,7 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     for (int e = 0; e < kM; ++e) tw[e] = make_float2((float)std::cos(kTwoPi * e / kM), (float)std::sin(kTwoPi * e / kM));
     // PFA path: conj(DFT_1023(chip)) / 1023 in float64, spectrum index k = (528 k1 + 496 k2)
     // mod 1023 stored at [k2][k1] (gacq_pfa.cuh); column 31 of each row is zero padding
-    std::vector<float2> ccp((size_t)c->n_prn * kBuf, make_float2(0.f, 0.f));
+    std::vector<float2> ccp((size_t)c->n_prn * kCcHalf, make_float2(0.f, 0.f));
     {
         std::vector<double> cs(kChips), sn(kChips);
         for (int m = 0; m < kChips; ++m) {
@@ -578,9 +578,10 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
                             re += chips[j] * cs[m];
                             im -= chips[j] * sn[m];
                         }
-                        // conj / 1023
-                        ccp[(size_t)i * kBuf + (k % 33) * 32 + k % 31] =
-                            make_float2((float)(re / kChips), (float)(-im / kChips));
+                        // conj / 1023; only the Hermitian half k2 <= 16 is kept
+                        if (k % 33 <= 16)
+                            ccp[(size_t)i * kCcHalf + (k % 33) * 32 + k % 31] =
+                                make_float2((float)(re / kChips), (float)(-im / kChips));
                     }
                 }
             });

@@ -22,15 +22,16 @@
 namespace gacq {
 
 constexpr int kBuf = 33 * 32;                    // spectrum [k2][32]; column 31 is padding
-constexpr int kScr = 34;                         // coop31 scratch (33 used; keeps 16 B alignment)
+constexpr int kScr = 34;                         // K1 coop31 scratch (33 used; keeps 16 B alignment)
 constexpr unsigned kSpecBytes = kBuf * sizeof(cx);
 constexpr int kCorrMaxWarps = 6;
-constexpr int kCorrWarpCx = 2 * kBuf + kScr;     // per-warp shared memory (cx)
+constexpr int kCorrWarpCx = 2 * kBuf;            // per-warp shared memory (cx): two spectra
+constexpr int kCcHalf = 17 * 32;                 // Hermitian half of a conj code spectrum (cx)
 #ifndef GACQ_PFA_MAXNREG
-#define GACQ_PFA_MAXNREG 208                     // no spills; 168 would give 12 warps/SM with spills
+#define GACQ_PFA_MAXNREG 168                     // 3 CTAs x 4 warps per SM; no spills (streamed stages)
 #endif
 
-__host__ __device__ constexpr int corr_pfa_smem(int W) { return W * (kCorrWarpCx * 8 + 16); }
+__host__ __device__ constexpr int corr_pfa_smem(int W) { return W * (kCorrWarpCx * 8 + 16) + kCcHalf * 8; }
 __host__ __device__ constexpr int fwd_pfa_smem(int D, int W) { return 8 * (D * fwd_ws(D) + W * (kBuf + kScr)); }
 
 // ---- bulk async copy + mbarrier (SASS UBLKCP / SYNCS) ------------------------------------
@@ -56,6 +57,10 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
             smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 __device__ __forceinline__ float pow_acc(cx v, float acc) { return fmaf(im(v), im(v), fmaf(re(v), re(v), acc)); }
@@ -153,7 +158,7 @@ __global__ void __launch_bounds__(32 * W) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
 // ---- K2 ---------------------------------------------------------------------------------
 struct CorrPfaArgs {
     const cx* Z;           // spectra of this chunk, [pairs][R][D][kBuf]
-    const cx* Cc;          // [n_prn][kBuf] conj code spectra / 1023, layout [k2][32]
+    const cx* Cc;          // [n_prn][kCcHalf] conj code spectra / 1023, rows k2 <= 16 of [k2][32]
     gacq_row* rows_bin;    // [n_snap][n_prn][B]
     float* pmap;           // optional [n_prn][B][P] power map (single snapshot), else null
     float* row_scratch;    // [gridDim][D][1023] native-order power rows when PW > 1
@@ -161,6 +166,7 @@ struct CorrPfaArgs {
     int64_t n_items;       // pairs_in_chunk * n_prn, item = lp * n_prn + pi
     unsigned long long* counter;  // zeroed before the launch
     int B, R, D, P, n_prn, radius, PW;
+    int zero;              // 0 (an opaque runtime zero, see dft31_stream)
 };
 
 // chip lag of cell (q1, q2)
@@ -176,85 +182,108 @@ __device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
 }
 
 // Persistent: gridDim.x = resident CTA slots of 32 W threads; CTA c starts with item c and
-// claims the following items in order from a global counter, so the CTAs sharing a pair's
-// spectra run together and hit them in L2. Warp w owns phases [w PW, w PW + PW) of the item.
+// claims the following items in order from a global counter (two items ahead, so the atomic
+// never stalls), so the CTAs sharing a pair's spectra run together and hit them in L2.
+// Warp w owns phases [w PW, w PW + PW) of the item. The item's conjugate code spectrum sits in
+// shared memory as the Hermitian half [17][32] (rows k2 > 16 are conj of row 33 - k2, lane
+// (31 - k1) mod 31), refilled with cp.async between items.
 // kRegs (PW == 1): the powers stay in registers through the argmax and the floor.
 // dynamic smem: corr_pfa_smem(W).
 template <bool kRegs>
 __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
     __shared__ float red_v[kCorrMaxWarps], red_f[kCorrMaxWarps];
     __shared__ int red_i[kCorrMaxWarps];
-    __shared__ long long s_next;
+    __shared__ long long s_claim;
     __shared__ float s_coef[15][32];  // coop31 columns, read conflict-free as s_coef[j-1][lane]
     extern __shared__ __align__(16) cx smem[];
     const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 15 * 32; i += blockDim.x) s_coef[i >> 5][i & 31] = coop31_coef(i & 31, (i >> 5) + 1);
-    __syncthreads();
     cx* buf = smem + w * kCorrWarpCx;  // buf[0..kBuf), buf[kBuf..2kBuf)
-    cx* scr = buf + 2 * kBuf;
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + W * kCorrWarpCx) + 2 * w;
+    cx* ccs = smem + W * kCorrWarpCx;  // [17][32] conj code spectrum half of the current item
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(ccs + kCcHalf) + 2 * w;
     if (lane == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
         fence_mbar_init();
     }
-    __syncwarp();
-
-    const int rho0 = w * a.PW;
-    const int n_tr = min(a.PW, a.D - rho0) * a.R;  // transforms of this warp per item
-    auto src = [&](int64_t item, int j) {
-        const int64_t lp = item / a.n_prn;
-        return a.Z + ((lp * a.R + j % a.R) * a.D + rho0 + j / a.R) * kBuf;
-    };
     int64_t item = blockIdx.x;
     if (item >= a.n_items) return;
+    auto load_cc = [&](int64_t it) {  // cp.async of the half spectrum of item `it`'s PRN
+        const char* g = reinterpret_cast<const char*>(a.Cc + (it % a.n_prn) * kCcHalf);
+        for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(ccs + 2 * i, g + 16 * i);
+        cp_async_commit();
+    };
+    if (threadIdx.x == 0) s_claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
+    load_cc(item);
+
+    const int rho0 = w * a.PW;
+    const int nph = min(a.PW, a.D - rho0);  // phases of this warp
+    const int64_t pair_span = (int64_t)a.R * a.D * kBuf;
+    auto zbase = [&](int64_t it) { return a.Z + (it / a.n_prn) * pair_span + rho0 * kBuf; };
     unsigned t = 0;  // this warp's transform count: buffer t & 1, mbarrier parity (t >> 1) & 1
-    if (lane == 0) bulk_load(buf, src(item, 0), kSpecBytes, &mbar[0]);
+    __syncwarp();
+    if (lane == 0) bulk_load(buf, zbase(item), kSpecBytes, &mbar[0]);
     float* rows = a.row_scratch + (int64_t)blockIdx.x * a.D * kChips;
+    const int pl = lane == 0 ? 0 : 31 - lane;  // Hermitian partner column of k1 = lane
+    cp_async_wait_all();
+    __syncthreads();
+    int64_t next = s_claim;
 
     for (;;) {
-        if (threadIdx.x == 0) s_next = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
-        __syncthreads();
-        const int64_t next = s_next;
+        long long claim = 0;
+        if (threadIdx.x == 0 && next < a.n_items) claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
         const int64_t lp = item / a.n_prn;
         const int pi = (int)(item % a.n_prn);
-        const cx* cc = a.Cc + (int64_t)pi * kBuf + lane;
+        const cx* zb = zbase(item);
+        const cx* zn = next < a.n_items ? zbase(next) : nullptr;
 
         float best = -1.f;
         int bidx = 0x7fffffff;
         float acc[31], accx[2];
+        int rd = 0, ph = 0;  // round and phase of the current transform
 #pragma unroll 1
-        for (int j = 0; j < n_tr; ++j, ++t) {
-            if (j % a.R == 0) {
+        for (;; ++t) {
+            if (rd == 0) {
 #pragma unroll
                 for (int i = 0; i < 31; ++i) acc[i] = 0.f;
                 accx[0] = accx[1] = 0.f;
             }
+            const bool last_rd = rd + 1 == a.R;
+            const bool last = last_rd && ph + 1 == nph;
             if (lane == 0) {  // prefetch the warp's next spectrum into the other buffer
-                const cx* nsrc = j + 1 < n_tr ? src(item, j + 1) : next < a.n_items ? src(next, 0) : nullptr;
+                const cx* nsrc = !last ? zb + ((last_rd ? 0 : rd + 1) * a.D + (last_rd ? ph + 1 : ph)) * kBuf : zn;
                 if (nsrc) bulk_load(buf + ((t + 1) & 1) * kBuf, nsrc, kSpecBytes, &mbar[(t + 1) & 1]);
             }
             mbar_wait(&mbar[t & 1], (t >> 1) & 1);
             cx* E = buf + (t & 1) * kBuf;
             // Z * Cc and the 33-point stage over k2; results E[q2][k1] written in place
-            cx x[33];
+            // (the 33-point stage reads all of E before the __syncwarp and writes after it)
             if (lane < 31) {
-#pragma unroll
-                for (int k2 = 0; k2 < 33; ++k2) x[k2] = cmul(E[k2 * 32 + lane], __ldg(cc + k2 * 32));
+                const cx* Ec = E + lane;
+                dft33_stream<1>(
+                    [&](int k2, int dep) {
+                        // k2 is a compile-time constant here: the branch folds away
+                        return k2 <= 16 ? cmul(Ec[k2 * 32 + dep], ccs[k2 * 32 + lane + dep])
+                                        : cmul_conj(Ec[k2 * 32 + dep], ccs[(33 - k2) * 32 + pl + dep]);
+                    },
+                    a.zero, [&](int q2, cx v) {
+                        if (q2 == 0) __syncwarp(0x7fffffffu);
+                        E[q2 * 31 + lane] = v;
+                    });
             }
             __syncwarp();
-            if (lane < 31) dft33<1>(x, [&](int q2, cx v) { E[q2 * 31 + lane] = v; });
-            __syncwarp();
-            // 31-point stage over k1 for row q2 = lane (+ row 32 spread over the warp)
+            // 31-point stage over k1 for row q2 = lane (+ row 32 spread over the warp, with its
+            // scratch in the buffer's unused tail E[1023..1055])
             const cx e = lane < 31 ? E[32 * 31 + lane] : czero();
             const cx* Er = E + lane * 31;
-            dft31_stream<1>([&](int k1) { return Er[k1]; }, [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
-            coop31<1>(e, lane, [&](int j) { return s_coef[j - 1][lane]; }, scr,
+            dft31_stream<1>([&](int k1, int dep) { return Er[k1 + dep]; }, a.zero,
+                            [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+            coop31<1>(e, lane, [&](int j) { return s_coef[j - 1][lane]; }, E + kChips,
                       [&](int sl, int, cx v) { accx[sl] = pow_acc(v, accx[sl]); });
             __syncwarp();  // E is free for the prefetch issued at the next transform
 
-            if (!kRegs && j % a.R == a.R - 1) {  // phase done: spill to the row, track the argmax
-                const int rho = rho0 + j / a.R;
+            if (!kRegs && last_rd) {  // phase done: spill to the row, track the argmax
+                const int rho = rho0 + ph;
                 float* row = rows + rho * kChips;
 #pragma unroll
                 for (int q1 = 0; q1 < 31; ++q1) {
@@ -273,6 +302,8 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                     }
                 }
             }
+            if (last) { ++t; break; }
+            if (last_rd) { rd = 0; ++ph; } else { ++rd; }
         }
         // cells of this lane (kRegs): (q1, lane) for q1 < 31, and coop cells
         auto for_cells = [&](auto&& f) {
@@ -294,7 +325,10 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
             if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
         }
         if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
-        __syncthreads();  // (also publishes the row spills of every warp)
+        if (threadIdx.x == 0) s_claim = claim;
+        __syncthreads();  // every warp is done with this item's spectra, Cc and row spills
+        const int64_t after = s_claim;
+        if (next < a.n_items) load_cc(next);  // lands while the floor is computed
         best = red_v[0];
         bidx = red_i[0];
         for (int i = 1; i < W; ++i)
@@ -323,7 +357,8 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
         if (lane == 0) red_f[w] = fl;
-        __syncthreads();
+        cp_async_wait_all();
+        __syncthreads();  // publishes red_f and the next item's Cc
         if (threadIdx.x == 0) {
             float f = red_f[0];
             for (int i = 1; i < W; ++i) f = fmaxf(f, red_f[i]);
@@ -335,6 +370,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
             a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
         }
         item = next;
+        next = after;
         if (item >= a.n_items) break;
     }
 }

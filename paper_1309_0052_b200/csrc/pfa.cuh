@@ -77,18 +77,27 @@ __device__ __forceinline__ void dft_odd(cx (&x)[P], Emit&& emit) {
     }
 }
 
-// Same transform for P = 31 with the inputs streamed: load(j) is called once per input, in the
-// order 0, (1, 30), (2, 29), ..., and each pair is folded into all 15 (A_k, B_k) accumulators
-// as soon as it arrives, so at most one input pair is live beside the 60 accumulator registers
-// (the unstreamed form keeps all 31 inputs and all 30 accumulators live at once).
+// Same transform for P = 31 with the inputs streamed: each input pair (j, 31-j) is folded into
+// all 15 (A_k, B_k) accumulators as it arrives, so only two pairs are live beside the 60
+// accumulator registers (the unstreamed form keeps all 31 inputs and all 30 accumulators live
+// at once). load(j, dep) must return input j and make its address depend on `dep`, which is
+// always 0 but carries the accumulators of step j-2: the scheduler then cannot hoist all loads
+// to the top, and each pair's load still overlaps one step of FFMA2s. `zero` must be a runtime
+// 0 the compiler cannot see through (a kernel argument).
 template <int S, typename Load, typename Emit>
-__device__ __forceinline__ void dft31_stream(Load&& load, Emit&& emit) {
+__device__ __forceinline__ void dft31_stream(Load&& load, int zero, Emit&& emit) {
     constexpr int P = 31, H = 15;
-    const cx x0 = load(0);
+    const cx x0 = load(0, 0);
     cx A[H], B[H], s0 = x0, s1 = czero();
+    cx nj = load(1, 0), nm = load(P - 1, 0);
 #pragma unroll
     for (int j = 1; j <= H; ++j) {
-        const cx xj = load(j), xm = load(P - j);
+        const cx xj = nj, xm = nm;
+        if (j < H) {
+            const int dep = j == 1 ? 0 : (int)(B[H - 1] >> 32) & zero;
+            nj = load(j + 1, dep);
+            nm = load(P - j - 1, dep);
+        }
         const cx a = add2(xj, xm), b = sub2(xj, xm);
         (j & 1 ? s1 : s0) = add2(j & 1 ? s1 : s0, a);
 #pragma unroll
@@ -113,6 +122,28 @@ __device__ __forceinline__ void dft33(cx (&x)[33], Emit&& emit) {
 #pragma unroll
     for (int b = 0; b < 11; ++b) {
         cx t[3] = {x[(3 * b) % 33], x[(11 + 3 * b) % 33], x[(22 + 3 * b) % 33]};
+        dft_odd<S, 3, 1>(t, [&](int c, cx v) { y[c][b] = v; });
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dft_odd<S, 11, 5>(y[c], [&](int e, cx v) { emit((22 * c + 12 * e) % 33, v); });
+}
+
+// dft33 with streamed inputs (see dft31_stream): the 3-point layer takes its triples
+// (3b, 11+3b, 22+3b) mod 33 in order b = 0..10, the next triple's loads depending on the
+// previous layer output, so the 11-point layer starts with only y[3][11] live.
+template <int S, typename Load, typename Emit>
+__device__ __forceinline__ void dft33_stream(Load&& load, int zero, Emit&& emit) {
+    cx y[3][11];
+    cx n0 = load(0, 0), n1 = load(11, 0), n2 = load(22, 0);
+#pragma unroll
+    for (int b = 0; b < 11; ++b) {
+        cx t[3] = {n0, n1, n2};
+        if (b < 10) {
+            const int dep = b == 0 ? 0 : (int)(y[2][b - 1] >> 32) & zero;
+            n0 = load((3 * b + 3) % 33, dep);
+            n1 = load((14 + 3 * b) % 33, dep);
+            n2 = load((25 + 3 * b) % 33, dep);
+        }
         dft_odd<S, 3, 1>(t, [&](int c, cx v) { y[c][b] = v; });
     }
 #pragma unroll
