@@ -52,6 +52,10 @@ CONFIGS = {
 }
 
 
+# dominant (K2) kernel of each device path, gacq_info.path
+KERNEL_NAMES = {1: "gacq_corr_kernel (2048-point chip-polyphase)", 2: "gacq_corr_pfa_kernel (1023-point prime-factor)"}
+
+
 def acq_kwargs(c):
     return dict(doppler_min_hz=-c["span_hz"], doppler_max_hz=c["span_hz"], doppler_step_hz=c["step"],
                 noncoherent_rounds=c["rounds"])
@@ -412,7 +416,7 @@ def run_ours(args, rank, world, local_rank):
                    "cells_per_step_per_gpu": cells_step, "fs_hz": c["fs"], "prns": 32, "bins": n_bins,
                    "parallelism": f"dp{world} (snapshot shards, no collective)",
                    "l2": f"inputs larger than L2 ({in_bytes / 2**20:.0f} MiB per GPU), no flush"},
-        "roofline": {"bound": "fp32", "kernel": "gacq_corr_kernel", "achieved": achieved, "peak": fp32_peak,
+        "roofline": {"bound": "fp32", "kernel": KERNEL_NAMES[eng.info["path"]], "achieved": achieved, "peak": fp32_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp32_peak if achieved else None,
                      "traffic": traffic,
                      "peak_source": f"nominal FP32 {sm} SMs x 128 lanes x 2 x {max_mhz:.0f} MHz "

@@ -74,11 +74,12 @@ typedef struct gacq_info {
     int32_t samples_per_period; /* P  = round(fs*1023/1.023e6) (acquisition.py:108-109) */
     int32_t n_coh;              /* samples per coherent block  (acquisition.py:116)     */
     int32_t chip_oversample;    /* D  = P / 1023 samples per chip                       */
-    int32_t fft_len;            /* M  = 2048 transform length on the device             */
+    int32_t fft_len;            /* transform length on the device: 1023 (path 2) or 2048 */
     int32_t n_bins;
     int32_t n_prn;
     int32_t rounds;
-    int32_t path;               /* 1 = chip-polyphase 2048-point path                   */
+    int32_t path;               /* 2 = 1023-point prime-factor path (default),
+                                   1 = chip-polyphase 2048-point path (GACQ_PATH=2048)  */
 } gacq_info;
 
 typedef struct gacq_stats {
