@@ -53,7 +53,8 @@ CONFIGS = {
 
 
 # dominant (K2) kernel of each device path, gacq_info.path
-KERNEL_NAMES = {1: "gacq_corr_kernel (2048-point chip-polyphase)", 2: "gacq_corr_pfa_kernel (1023-point prime-factor)"}
+KERNEL_NAMES = {1: "gacq_corr_kernel (2048-point chip-polyphase)", 2: "gacq_corr_pfa_kernel (1023-point prime-factor)",
+                3: "gacq_corr_tc_kernel (1023-point prime-factor, 31-point stage on tcgen05)"}
 
 
 def acq_kwargs(c):

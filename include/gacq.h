@@ -79,7 +79,9 @@ typedef struct gacq_info {
     int32_t n_prn;
     int32_t rounds;
     int32_t path;               /* 2 = 1023-point prime-factor path (default),
-                                   1 = chip-polyphase 2048-point path (GACQ_PATH=2048)  */
+                                   1 = chip-polyphase 2048-point path (GACQ_PATH=2048),
+                                   3 = path 2 with the 31-point stage on the tensor cores */
+    int32_t corr_ctas;          /* persistent K2 grid (resident CTAs on the device)      */
 } gacq_info;
 
 typedef struct gacq_stats {

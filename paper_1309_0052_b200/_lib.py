@@ -30,7 +30,7 @@ class Row(C.Structure):
 
 class Info(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("samples_per_period", "n_coh", "chip_oversample", "fft_len",
-                                         "n_bins", "n_prn", "rounds", "path")]
+                                         "n_bins", "n_prn", "rounds", "path", "corr_ctas")]
 
 
 class Stats(C.Structure):

@@ -24,6 +24,7 @@
 
 #include "gacq_kernels.cuh"
 #include "gacq_pfa.cuh"
+#include "gacq_tc.cuh"
 #include "gtrk_kernels.cuh"
 
 using namespace gacq;
@@ -121,7 +122,9 @@ struct gacq_ctx {
     int ng = 1;  // K1 transform groups per CTA (2048-point path)
     bool pfa = true;  // 1023-point prime-factor path (gacq_pfa.cuh); GACQ_PATH=2048 selects the other
     int cw = 4, cpw = 1;  // PFA K2: warps per CTA, phases per warp
+    bool tc = false;      // PFA K2 with the 31-point stage on the tensor cores (gacq_tc.cuh)
     float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kBuf]
+    float* d_tcB = nullptr;   // tensor-core 31-point inverse DFT matrix, hi and lo [2][64*64]
     std::vector<double> bins;
     std::vector<int32_t> prns;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -228,6 +231,14 @@ void corr_pfa_shape(int D, int* W, int* PW) {
 
 cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
+    if (c->tc) {
+        const float4* B = reinterpret_cast<const float4*>(c->d_tcB);
+        if (c->cpw == 1)
+            gacq_corr_tc_kernel<true><<<(unsigned)blocks, 32 * kTcWarps, corr_tc_smem(), c->stream>>>(ca, B);
+        else
+            gacq_corr_tc_kernel<false><<<(unsigned)blocks, 32 * kTcWarps, corr_tc_smem(), c->stream>>>(ca, B);
+        return cudaGetLastError();
+    }
     if (c->cpw == 1)
         gacq_corr_pfa_kernel<true><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
     else
@@ -428,6 +439,7 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_tw);
         cudaFree(c->d_Z);
         cudaFree(c->d_ccp);
+        cudaFree(c->d_tcB);
         cudaFree(c->d_in);
         cudaFree(c->d_raw);
         cudaFree(c->d_rows_bin);
@@ -517,6 +529,15 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->ng = D >= 2 ? 2 : 1;
     if (const char* ev = std::getenv("GACQ_PATH")) c->pfa = std::strcmp(ev, "2048") != 0;
     corr_pfa_shape(D, &c->cw, &c->cpw);
+    {
+        const char* ev = std::getenv("GACQ_TC");
+        // opt-in (GACQ_TC=1): measured slower than the FP32 kernel on B200, see DESIGN.md section 5
+        c->tc = c->pfa && D % kTcWarps == 0 && ev && std::strcmp(ev, "1") == 0;
+        if (c->tc) {
+            c->cw = kTcWarps;
+            c->cpw = D / kTcWarps;
+        }
+    }
     c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
     c->prns.assign(p->prns, p->prns + p->n_prn);
 
@@ -588,6 +609,29 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         for (auto& t : th) t.join();
     }
 
+    // tensor-core 31-point inverse DFT (gacq_tc.cuh): B[2 k1 + c][2 q1 + c'] is the real form of
+    // exp(+2 pi i k1 q1 / 31), stored as [n = 2 q1 + c'][k = 2 k1 + c] in core-matrix order, split
+    // into hi (top 19 bits, what TF32 reads) and lo = B - hi
+    std::vector<float> tcB(2 * kTcB, 0.f);
+    for (int k1 = 0; k1 < 31; ++k1)
+        for (int q1 = 0; q1 < 31; ++q1) {
+            const double th = kTwoPi * (double)((k1 * q1) % 31) / 31.0;
+            const float cs = (float)std::cos(th), sn = (float)std::sin(th);
+            const float val[2][2] = {{cs, sn}, {-sn, cs}};  // [c][c']: re/im of the input x re/im of the output
+            for (int cc = 0; cc < 2; ++cc)
+                for (int co = 0; co < 2; ++co) {
+                    const float b = val[cc][co];
+                    uint32_t u;
+                    std::memcpy(&u, &b, 4);
+                    u &= 0xffffe000u;
+                    float hi;
+                    std::memcpy(&hi, &u, 4);
+                    const int off = tc_b_off(2 * q1 + co, 2 * k1 + cc);
+                    tcB[off] = hi;
+                    tcB[kTcB + off] = b - hi;
+                }
+        }
+
     // ---- device state ---------------------------------------------------------------
     DeviceGuard guard(c->device);
     auto bail = [&](int code) {
@@ -613,6 +657,16 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
+    if (c->tc) {
+        CTX_TRY(cudaMalloc(&c->d_tcB, tcB.size() * sizeof(float)));
+        CTX_TRY(cudaMemcpy(c->d_tcB, tcB.data(), tcB.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     corr_tc_smem()));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     corr_tc_smem()));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
     if (c->pfa) {
         // every PFA variant gets the largest dynamic shared memory any plan launches it with
         CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -625,13 +679,18 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         GACQ_PFA_FWD_VARIANTS(GACQ_ATTR_FWDP)
 #undef GACQ_ATTR_FWDP
         int per_sm = 0, sms = 0;
-        if (c->cpw == 1)
+        if (c->tc)
+            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->cpw == 1 ? gacq_corr_tc_kernel<true>
+                                                                                    : gacq_corr_tc_kernel<false>,
+                                                                  32 * kTcWarps, corr_tc_smem()));
+        else if (c->cpw == 1)
             CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<true>, 32 * c->cw,
                                                                   corr_pfa_smem(c->cw)));
         else
             CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<false>, 32 * c->cw,
                                                                   corr_pfa_smem(c->cw)));
         CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+        if (const char* ev = std::getenv("GACQ_CORR_CTAS_PER_SM")) per_sm = std::atoi(ev);
         c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
         if (c->cpw > 1)
             CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kChips * sizeof(float)));
@@ -679,7 +738,8 @@ int gacq_info_get(const gacq_ctx* c, gacq_info* o) {
     o->n_bins = c->B;
     o->n_prn = c->n_prn;
     o->rounds = c->R;
-    o->path = c->pfa ? 2 : 1;
+    o->path = c->tc ? 3 : c->pfa ? 2 : 1;
+    o->corr_ctas = (int32_t)c->corr_slots;
     return GACQ_OK;
 }
 
