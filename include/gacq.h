@@ -135,6 +135,11 @@ int gacq_run_quantized(gacq_ctx* ctx, const void* iq, int32_t sample_format, dou
  * snapshot (the reference's power_map, acquisition.py:131-149). */
 int gacq_power_map(gacq_ctx* ctx, const void* snap_host, float* out_host);
 
+/* Parity hook: the plan's carrier table [n_bins][n_coh] complex64, built on the device
+ * and bit-identical to carrier_replica(NcoState(), f, fs, n_coh)
+ * (gnss_signal.py:49-72 -> kernels.py:106-114) for every bin f. */
+int gacq_carrier_table(gacq_ctx* ctx, void* out_host);
+
 int gacq_stats_get(const gacq_ctx* ctx, gacq_stats* out);
 int gacq_stats_reset(gacq_ctx* ctx);
 

@@ -288,6 +288,12 @@ class AcqEngine:
     def search_quantized(self, iq, sample_format: int, scale: float, profile: bool = False) -> BatchResult:
         return self.finish(self.run_rows_quantized(iq, sample_format, scale, profile=profile))
 
+    def carrier_table(self) -> np.ndarray:
+        """complex64 [n_bins, n_coh] wipe-off replicas the device built (parity hook)."""
+        out = np.empty((self.bins.size, self.info["n_coh"]), dtype=np.complex64)
+        _lib.check(_lib.lib.gacq_carrier_table(self._ctx, out.ctypes.data))
+        return out
+
     def power_map(self, snapshot) -> np.ndarray:
         """float32 [n_prn, n_bins, P] noncoherent power of one host snapshot (parity hook)."""
         arr = _host_array(snapshot)

@@ -25,6 +25,7 @@
 #include "gacq_kernels.cuh"
 #include "gacq_pfa.cuh"
 #include "gacq_tc.cuh"
+#include "gacq_tables.cuh"
 #include "gtrk_kernels.cuh"
 
 using namespace gacq;
@@ -541,72 +542,33 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
     c->prns.assign(p->prns, p->prns + p->n_prn);
 
-    // ---- host tables --------------------------------------------------------------
-    // carrier replicas, bit-identical to kernels.py:106-114 (phase 0, acquisition.py:139)
-    std::vector<float2> carrier((size_t)c->B * n_coh);
-    {
-        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 16));
-        std::vector<std::thread> th;
-        for (int w = 0; w < nt; ++w)
-            th.emplace_back([&, w]() {
-                for (int b = w; b < c->B; b += nt) {
-                    const int64_t step = py_mod(py_round((c->bins[b] / fs) * (double)kCarrierScale), kCarrierScale);
-                    const double inv = kTwoPi / (double)kCarrierScale;
-                    float2* o = carrier.data() + (size_t)b * n_coh;
-                    for (int64_t k = 0; k < n_coh; ++k) {
-                        const uint64_t ph = ((uint64_t)k * (uint64_t)step) & (uint64_t)(kCarrierScale - 1);
-                        const double th = (double)ph * inv;
-                        o[k] = make_float2((float)std::cos(th), (float)(-std::sin(th)));
-                    }
-                }
-            });
-        for (auto& t : th) t.join();
-    }
-    // conjugate code spectra / 2048 of d[j] = chip[j mod 1023], j < 2046
-    std::vector<float2> cc((size_t)c->n_prn * kM);
-    for (int i = 0; i < c->n_prn; ++i) {
-        int8_t chips[1023];
-        ca_code(c->prns[i], chips);
-        std::vector<std::complex<double>> d(kM, 0.0);
-        for (int j = 0; j < 2 * 1023; ++j) d[j] = (double)chips[j % 1023];
-        fft_f64(d);
-        for (int k = 0; k < kM; ++k) {
-            const auto v = std::conj(d[k]) / (double)kM;
-            cc[(size_t)i * kM + perm_slot(k)] = make_float2((float)v.real(), (float)v.imag());
+    // ---- tables ---------------------------------------------------------------------
+    // Built on the device (gacq_tables.cuh): carrier replicas bit-identical to
+    // kernels.py:106-114 at phase 0 (acquisition.py:139), C/A chips and the conjugate code
+    // spectra. The host only resolves the per-bin 48-bit NCO steps (kernels.py:61-62) exactly
+    // as Python does (round-half-even, floor modulo).
+    std::vector<uint64_t> steps(c->B);
+    for (int b = 0; b < c->B; ++b)
+        steps[b] = (uint64_t)py_mod(py_round((c->bins[b] / fs) * (double)kCarrierScale), kCarrierScale);
+    // 2048-point path (GACQ_PATH=2048) tables: conjugate code spectra / 2048 of
+    // d[j] = chip[j mod 1023], j < 2046, in the permuted layout, and twiddles
+    std::vector<float2> cc, tw;
+    if (!c->pfa) {
+        cc.resize((size_t)c->n_prn * kM);
+        for (int i = 0; i < c->n_prn; ++i) {
+            int8_t chips[1023];
+            ca_code(c->prns[i], chips);
+            std::vector<std::complex<double>> d(kM, 0.0);
+            for (int j = 0; j < 2 * 1023; ++j) d[j] = (double)chips[j % 1023];
+            fft_f64(d);
+            for (int k = 0; k < kM; ++k) {
+                const auto v = std::conj(d[k]) / (double)kM;
+                cc[(size_t)i * kM + perm_slot(k)] = make_float2((float)v.real(), (float)v.imag());
+            }
         }
-    }
-    std::vector<float2> tw(kM);
-    for (int e = 0; e < kM; ++e) tw[e] = make_float2((float)std::cos(kTwoPi * e / kM), (float)std::sin(kTwoPi * e / kM));
-    // PFA path: conj(DFT_1023(chip)) / 1023 in float64, spectrum index k = (528 k1 + 496 k2)
-    // mod 1023 stored at [k2][k1] (gacq_pfa.cuh); column 31 of each row is zero padding
-    std::vector<float2> ccp((size_t)c->n_prn * kCcHalf, make_float2(0.f, 0.f));
-    {
-        std::vector<double> cs(kChips), sn(kChips);
-        for (int m = 0; m < kChips; ++m) {
-            cs[m] = std::cos(kTwoPi * m / kChips);
-            sn[m] = std::sin(kTwoPi * m / kChips);
-        }
-        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 16));
-        std::vector<std::thread> th;
-        for (int w = 0; w < nt; ++w)
-            th.emplace_back([&, w]() {
-                for (int i = w; i < c->n_prn; i += nt) {
-                    int8_t chips[kChips];
-                    ca_code(c->prns[i], chips);
-                    for (int k = 0; k < kChips; ++k) {
-                        double re = 0, im = 0;
-                        for (int j = 0, m = 0; j < kChips; ++j, m = m + k >= kChips ? m + k - kChips : m + k) {
-                            re += chips[j] * cs[m];
-                            im -= chips[j] * sn[m];
-                        }
-                        // conj / 1023; only the Hermitian half k2 <= 16 is kept
-                        if (k % 33 <= 16)
-                            ccp[(size_t)i * kCcHalf + (k % 33) * 32 + k % 31] =
-                                make_float2((float)(re / kChips), (float)(-im / kChips));
-                    }
-                }
-            });
-        for (auto& t : th) t.join();
+        tw.resize(kM);
+        for (int e = 0; e < kM; ++e)
+            tw[e] = make_float2((float)std::cos(kTwoPi * e / kM), (float)std::sin(kTwoPi * e / kM));
     }
 
     // tensor-core 31-point inverse DFT (gacq_tc.cuh): B[2 k1 + c][2 q1 + c'] is the real form of
@@ -645,14 +607,45 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     } while (0)
     CTX_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CTX_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    CTX_TRY(cudaMalloc(&c->d_carrier, carrier.size() * sizeof(float2)));
-    CTX_TRY(cudaMalloc(&c->d_cc, cc.size() * sizeof(float2)));
-    CTX_TRY(cudaMalloc(&c->d_tw, tw.size() * sizeof(float2)));
-    CTX_TRY(cudaMemcpy(c->d_carrier, carrier.data(), carrier.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    CTX_TRY(cudaMemcpy(c->d_cc, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    CTX_TRY(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    CTX_TRY(cudaMalloc(&c->d_ccp, ccp.size() * sizeof(float2)));
-    CTX_TRY(cudaMemcpy(c->d_ccp, ccp.data(), ccp.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    {   // device tables; the temporaries are freed before returning
+        const size_t n_car = (size_t)c->B * n_coh;
+        CTX_TRY(cudaMalloc(&c->d_carrier, n_car * sizeof(float2)));
+        CTX_TRY(cudaMalloc(&c->d_ccp, (size_t)c->n_prn * kCcHalf * sizeof(float2)));
+        uint64_t* d_steps = nullptr;
+        int32_t* d_prns = nullptr;
+        int8_t* d_chips = nullptr;
+        auto tables = [&]() -> cudaError_t {
+            cudaError_t e;
+            if ((e = cudaMalloc(&d_steps, steps.size() * sizeof(uint64_t))) ||
+                (e = cudaMalloc(&d_prns, c->prns.size() * sizeof(int32_t))) ||
+                (e = cudaMalloc(&d_chips, (size_t)c->n_prn * kChips)))
+                return e;
+            if ((e = cudaMemcpyAsync(d_steps, steps.data(), steps.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                     c->stream)) ||
+                (e = cudaMemcpyAsync(d_prns, c->prns.data(), c->prns.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                     c->stream)) ||
+                (e = cudaMemsetAsync(c->d_ccp, 0, (size_t)c->n_prn * kCcHalf * sizeof(float2), c->stream)))
+                return e;
+            gacq_carrier_kernel<<<(unsigned)std::min<size_t>((n_car + 255) / 256, 148 * 16), 256, 0, c->stream>>>(
+                d_steps, c->B, (int)n_coh, kTwoPi / (double)kCarrierScale, c->d_carrier);
+            gacq_ca_chips_kernel<<<1, 32, 0, c->stream>>>(d_prns, c->n_prn, d_chips);
+            gacq_code_spectrum_kernel<<<(unsigned)((c->n_prn * kChips * 32 + 255) / 256), 256, 0, c->stream>>>(
+                d_chips, c->n_prn, reinterpret_cast<float2*>(c->d_ccp));
+            if ((e = cudaGetLastError())) return e;
+            return cudaStreamSynchronize(c->stream);
+        };
+        const cudaError_t te = tables();
+        cudaFree(d_steps);
+        cudaFree(d_prns);
+        cudaFree(d_chips);
+        CTX_TRY(te);
+    }
+    if (!c->pfa) {
+        CTX_TRY(cudaMalloc(&c->d_cc, cc.size() * sizeof(float2)));
+        CTX_TRY(cudaMalloc(&c->d_tw, tw.size() * sizeof(float2)));
+        CTX_TRY(cudaMemcpy(c->d_cc, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CTX_TRY(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    }
     const int64_t pair_bytes = (int64_t)c->R * c->D * (c->pfa ? kBuf : kM) * (int64_t)sizeof(float2);
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
@@ -793,6 +786,14 @@ int gacq_power_map(gacq_ctx* c, const void* snap, float* out) {
     int rc = run_impl(c, in, 1, true, false, nullptr, false, c->d_pmap);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpy(out, c->d_pmap, n * sizeof(float), cudaMemcpyDeviceToHost));
+    return GACQ_OK;
+}
+
+int gacq_carrier_table(gacq_ctx* c, void* out) {
+    if (!c || !out) return fail(GACQ_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaMemcpy(out, c->d_carrier, (size_t)c->B * c->n_coh * sizeof(float2), cudaMemcpyDeviceToHost));
     return GACQ_OK;
 }
 
