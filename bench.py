@@ -47,6 +47,9 @@ CONFIGS = {
                desc="C2: 10 ms snapshots @4.092 MHz, 32 PRNs x 41 bins (+-5 kHz/250 Hz), 10 x 1 ms noncoherent"),
     "c3": dict(fs=4.092e6, rounds=10, step=500.0, span_hz=5000.0, batch=1024,
                desc="C3: 10 ms snapshots @4.092 MHz, 32 PRNs x 21 bins (+-5 kHz/500 Hz), 10 x 1 ms noncoherent"),
+    "g5": dict(fs=5.0e6, rounds=10, step=500.0, span_hz=5000.0, batch=64,
+               desc="G5: 10 ms snapshots @5 MHz (not chip-aligned: generic power-of-two path), 32 PRNs x 21 bins, "
+                    "10 x 1 ms noncoherent"),
     "c4": dict(fs=16.368e6, rounds=20, step=125.0, span_hz=10000.0, batch=16,
                desc="C4: 20 ms snapshots @16.368 MHz, 32 PRNs x 161 bins (+-10 kHz/125 Hz), 20 x 1 ms noncoherent"),
 }
@@ -54,7 +57,8 @@ CONFIGS = {
 
 # dominant (K2) kernel of each device path, gacq_info.path
 KERNEL_NAMES = {1: "gacq_corr_kernel (2048-point chip-polyphase)", 2: "gacq_corr_pfa_kernel (1023-point prime-factor)",
-                3: "gacq_corr_tc_kernel (1023-point prime-factor, 31-point stage on tcgen05)"}
+                3: "gacq_corr_tc_kernel (1023-point prime-factor, 31-point stage on tcgen05)",
+                4: "gacq_gen_corr_kernel (generic power-of-two path)"}
 
 
 def acq_kwargs(c):
@@ -188,7 +192,6 @@ def synth_batch(torch, n, c, seed, device):
     from paper_1309_0052_b200 import generate_ca_code
 
     fs = c["fs"]
-    d = round(fs / 1.023e6)
     span = round(fs * 1e-3) * c["rounds"]
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -205,11 +208,11 @@ def synth_batch(torch, n, c, seed, device):
         for _ in range(8):
             prn = torch.randint(0, 32, (m,), generator=g, device=device)
             dop = (torch.rand((m,), generator=g, device=device, dtype=torch.float64) * 2 - 1) * (c["span_hz"] - 250)
-            cph = torch.randint(0, 1023 * d, (m,), generator=g, device=device)
+            cph = torch.randint(0, round(fs * 1e-3), (m,), generator=g, device=device)
             carr = torch.rand((m,), generator=g, device=device, dtype=torch.float64)
             cn0 = 38.0 + 10.0 * torch.rand((m,), generator=g, device=device, dtype=torch.float64)
             amp = (10.0 ** ((cn0 - 45.0) / 20.0)).to(torch.float32)
-            ci = torch.div(idx[None, :] - cph[:, None], d, rounding_mode="floor").remainder(1023)
+            ci = torch.div((idx[None, :] - cph[:, None]) * 1023000, round(fs), rounding_mode="floor").remainder(1023)
             code = chips[prn[:, None], ci]
             ph = torch.frac(dop[:, None] * idx[None, :].double() / fs + carr[:, None]) * (2 * math.pi)
             x += (amp[:, None] * code) * torch.polar(torch.ones_like(ph, dtype=torch.float32), ph.float())

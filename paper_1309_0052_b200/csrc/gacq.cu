@@ -26,6 +26,7 @@
 #include "gacq_pfa.cuh"
 #include "gacq_tc.cuh"
 #include "gacq_tables.cuh"
+#include "gacq_generic.cuh"
 #include "gtrk_kernels.cuh"
 
 using namespace gacq;
@@ -126,6 +127,10 @@ struct gacq_ctx {
     bool tc = false;      // PFA K2 with the 31-point stage on the tensor cores (gacq_tc.cuh)
     float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kBuf]
     float* d_tcB = nullptr;   // tensor-core 31-point inverse DFT matrix, hi and lo [2][64*64]
+    bool gen = false;         // generic power-of-two path (rates that are not chip-aligned)
+    int logM = 0;             // its transform length M = 2^logM >= n_coh + P - 1
+    float2* d_gtw = nullptr;  // [M/2] (cos, sin)(2 pi e / M)
+    float2* d_gcc = nullptr;  // [n_prn][M] conj(DFT_M(code replica)) / M
     std::vector<double> bins;
     std::vector<int32_t> prns;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -366,7 +371,17 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         }
         cx* Zp = reinterpret_cast<cx*>(c->d_Z);
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
-        if (c->pfa) {
+        GenArgs ga{in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
+                   pmap, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
+        const int gen_l = c->logM > kGenMaxLogM ? 2 : 1;
+        const int gen_smem = ((int)sizeof(float2) << c->logM) / gen_l;
+        if (c->gen) {
+            if (gen_l == 2)
+                gacq_gen_fwd_kernel<2><<<(unsigned)(np * c->R * 2), kGenThreads, gen_smem, c->stream>>>(ga);
+            else
+                gacq_gen_fwd_kernel<1><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
+            CUDA_TRY(cudaGetLastError());
+        } else if (c->pfa) {
             FwdPfaArgs fa{in, in_stride, c->d_carrier, Zp, p0, c->B, c->R, c->n_coh, c->P, c->K};
             CUDA_TRY(launch_fwd_pfa(c, fa, np * c->R));
         } else {
@@ -374,9 +389,15 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             CUDA_TRY(launch_fwd(c, fa, np * c->R));
         }
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
-        CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
+        if (!c->gen) CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
-        if (c->pfa) {
+        if (c->gen) {
+            if (gen_l == 2)
+                gacq_gen_corr_kernel<2><<<(unsigned)(np * c->n_prn), kGenThreads, gen_smem, c->stream>>>(ga);
+            else
+                gacq_gen_corr_kernel<1><<<(unsigned)(np * c->n_prn), kGenThreads, gen_smem, c->stream>>>(ga);
+            CUDA_TRY(cudaGetLastError());
+        } else if (c->pfa) {
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
                            np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw, 0};
             CUDA_TRY(launch_corr_pfa(c, ca));
@@ -441,6 +462,8 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_Z);
         cudaFree(c->d_ccp);
         cudaFree(c->d_tcB);
+        cudaFree(c->d_gtw);
+        cudaFree(c->d_gcc);
         cudaFree(c->d_in);
         cudaFree(c->d_raw);
         cudaFree(c->d_rows_bin);
@@ -491,24 +514,31 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     const int64_t n_coh = py_round(fs * p->coherent_ms * 1e-3);        // acquisition.py:116
     const int64_t P = py_round(fs * 1023.0 / kChipRate);              // acquisition.py:108-109
     if (n_coh < P) return fail(GACQ_ERR_INVALID, "coherent window shorter than one code period");
-    // chip-aligned structure required by the device algorithm
-    if (P % 1023 != 0 || n_coh % P != 0)
-        return fail(GACQ_ERR_UNSUPPORTED,
-                    "fs=%.17g Hz: the GPU path needs fs = D*1.023 MHz (integer D) and n_coh a multiple of the "
-                    "code period (got P=%lld, n_coh=%lld)", fs, (long long)P, (long long)n_coh);
-    const int D = (int)(P / 1023), K = (int)(n_coh / P);
-    if (!fwd_supported(D))
-        return fail(GACQ_ERR_UNSUPPORTED, "chip oversampling D=%d (fs=%.17g Hz) has no device variant", D, fs);
-    {   // the reference's replica must index chips exactly as floor(n/D) mod 1023 (kernels.py:116-128)
-        const int64_t step = py_round((kChipRate / fs) * (double)kCodeScale);
+    // Chip-aligned rates (fs = D * 1.023 MHz with the code NCO indexing chips exactly as
+    // floor(n / D) mod 1023, kernels.py:116-128) take the 1023-point path; every other rate
+    // takes the generic power-of-two path (gacq_generic.cuh).
+    const int64_t code_step = py_round((kChipRate / fs) * (double)kCodeScale);
+    bool aligned = P % 1023 == 0 && n_coh % P == 0 && fwd_supported((int)(P / 1023));
+    if (aligned) {
+        const int64_t Dl = P / 1023;
         int64_t ph = 0;
-        for (int64_t n = 0; n < n_coh; ++n) {
-            if ((ph >> 42) != (n / D) % 1023)
-                return fail(GACQ_ERR_UNSUPPORTED, "code NCO at fs=%.17g Hz is not chip-aligned at sample %lld", fs,
-                            (long long)n);
-            ph = (ph + step) % kCodeModulus;
+        for (int64_t n = 0; n < n_coh && aligned; ++n) {
+            aligned = (ph >> 42) == (n / Dl) % 1023;
+            ph = (ph + code_step) % kCodeModulus;
         }
     }
+    const char* path_env = std::getenv("GACQ_PATH");
+    const bool gen = !aligned || (path_env && std::strcmp(path_env, "generic") == 0);
+    int logM = 0;
+    if (gen) {
+        while ((int64_t(1) << logM) < n_coh + P - 1) ++logM;
+        if (logM > kGenMaxLogMTotal)
+            return fail(GACQ_ERR_UNSUPPORTED,
+                        "fs=%.17g Hz, coherent_ms=%d: the generic path's transform (%lld points >= n_coh + P - 1) "
+                        "exceeds %d; chip-aligned rates (fs = D*1.023 MHz) have no limit",
+                        fs, p->coherent_ms, (long long)(int64_t(1) << logM), 2 * kGenMaxM);
+    }
+    const int D = gen ? 0 : (int)(P / 1023), K = gen ? 0 : (int)(n_coh / P);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -529,7 +559,10 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->radius = p->exclusion_radius_samples ? p->exclusion_radius_samples : (int)std::ceil(fs / kChipRate);
     c->ng = D >= 2 ? 2 : 1;
     if (const char* ev = std::getenv("GACQ_PATH")) c->pfa = std::strcmp(ev, "2048") != 0;
-    corr_pfa_shape(D, &c->cw, &c->cpw);
+    c->gen = gen;
+    c->logM = logM;
+    if (gen) c->pfa = false;
+    if (!gen) corr_pfa_shape(D, &c->cw, &c->cpw);
     {
         const char* ev = std::getenv("GACQ_TC");
         // opt-in (GACQ_TC=1): measured slower than the FP32 kernel on B200, see DESIGN.md section 5
@@ -553,7 +586,7 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     // 2048-point path (GACQ_PATH=2048) tables: conjugate code spectra / 2048 of
     // d[j] = chip[j mod 1023], j < 2046, in the permuted layout, and twiddles
     std::vector<float2> cc, tw;
-    if (!c->pfa) {
+    if (!c->pfa && !gen) {
         cc.resize((size_t)c->n_prn * kM);
         for (int i = 0; i < c->n_prn; ++i) {
             int8_t chips[1023];
@@ -593,6 +626,43 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
                     tcB[kTcB + off] = b - hi;
                 }
         }
+
+    // generic path: conj(DFT_M(c)) / M of each PRN's sampled code replica c[n], n < n_coh,
+    // chip index (k * step mod 1023*2^42) >> 42 (kernels.py:116-128, acquisition.py:88-105),
+    // in float64 then rounded once; twiddles (cos, sin)(2 pi e / M)
+    std::vector<float2> gcc, gtw;
+    if (gen) {
+        const int M = 1 << logM;
+        gcc.resize((size_t)c->n_prn * M);
+        gtw.resize(M / 2);
+        for (int e = 0; e < M / 2; ++e)
+            gtw[e] = make_float2((float)std::cos(kTwoPi * e / M), (float)std::sin(kTwoPi * e / M));
+        std::vector<int32_t> idx(n_coh);
+        for (int64_t n = 0, ph = 0; n < n_coh; ++n) {
+            idx[n] = (int32_t)(ph >> 42);
+            ph += code_step;
+            if (ph >= kCodeModulus) ph -= kCodeModulus;
+        }
+        const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), c->n_prn));
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t]() {
+                std::vector<std::complex<double>> d(M);
+                int8_t chips[1023];
+                for (int i = t; i < c->n_prn; i += nt) {
+                    ca_code(c->prns[i], chips);
+                    std::fill(d.begin(), d.end(), 0.0);
+                    for (int64_t n = 0; n < n_coh; ++n) d[n] = (double)chips[idx[n]];
+                    fft_f64(d);
+                    const int L = M > kGenMaxM ? 2 : 1, Ms = M / L;  // residue-major (gacq_generic.cuh)
+                    for (int k = 0; k < M; ++k) {
+                        const auto v = std::conj(d[k]) / (double)M;
+                        gcc[(size_t)i * M + (k % L) * Ms + k / L] = make_float2((float)v.real(), (float)v.imag());
+                    }
+                }
+            });
+        for (auto& x : th) x.join();
+    }
 
     // ---- device state ---------------------------------------------------------------
     DeviceGuard guard(c->device);
@@ -640,16 +710,35 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         cudaFree(d_chips);
         CTX_TRY(te);
     }
-    if (!c->pfa) {
+    if (!c->pfa && !gen) {
         CTX_TRY(cudaMalloc(&c->d_cc, cc.size() * sizeof(float2)));
         CTX_TRY(cudaMalloc(&c->d_tw, tw.size() * sizeof(float2)));
         CTX_TRY(cudaMemcpy(c->d_cc, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
     }
-    const int64_t pair_bytes = (int64_t)c->R * c->D * (c->pfa ? kBuf : kM) * (int64_t)sizeof(float2);
+    if (gen) {
+        CTX_TRY(cudaMalloc(&c->d_gcc, gcc.size() * sizeof(float2)));
+        CTX_TRY(cudaMalloc(&c->d_gtw, gtw.size() * sizeof(float2)));
+        CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kGenMaxM * (int)sizeof(float2)));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kGenMaxM * (int)sizeof(float2)));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kGenMaxM * (int)sizeof(float2)));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kGenMaxM * (int)sizeof(float2)));
+    }
+    const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * (c->pfa ? kBuf : kM)) *
+                               (int64_t)sizeof(float2);
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
+    if (gen) {
+        *out = c;
+        return GACQ_OK;
+    }
     if (c->tc) {
         CTX_TRY(cudaMalloc(&c->d_tcB, tcB.size() * sizeof(float)));
         CTX_TRY(cudaMemcpy(c->d_tcB, tcB.data(), tcB.size() * sizeof(float), cudaMemcpyHostToDevice));
@@ -727,11 +816,11 @@ int gacq_info_get(const gacq_ctx* c, gacq_info* o) {
     o->samples_per_period = c->P;
     o->n_coh = c->n_coh;
     o->chip_oversample = c->D;
-    o->fft_len = c->pfa ? kChips : kM;
+    o->fft_len = c->gen ? (1 << c->logM) : c->pfa ? kChips : kM;
     o->n_bins = c->B;
     o->n_prn = c->n_prn;
     o->rounds = c->R;
-    o->path = c->tc ? 3 : c->pfa ? 2 : 1;
+    o->path = c->gen ? 4 : c->tc ? 3 : c->pfa ? 2 : 1;
     o->corr_ctas = (int32_t)c->corr_slots;
     return GACQ_OK;
 }

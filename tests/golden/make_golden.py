@@ -113,6 +113,8 @@ FS8 = 8.184e6
 
 
 def main():
+    if "--generic" in sys.argv:
+        return main_generic()
     t0 = time.time()
     cases = []
     maps = {}
@@ -233,6 +235,56 @@ def main():
         cases=cases), indent=1))
     np.savez_compressed(OUT / "maps.npz", **maps)
     print("wrote", len(cases), "cases,", len(maps), "maps in", round(time.time() - t0, 1), "s")
+
+
+def main_generic():
+    """Sample rates that are not chip-aligned (fs != D * 1.023 MHz): the reference's native
+    length is not a multiple of 1023, so the device runs its generic power-of-two path.
+    Writes tests/golden/golden_generic.json and maps_generic.npz."""
+    t0 = time.time()
+    cases = []
+    maps = {}
+
+    def add(name, kind, spec, buf, prns, cfg, keep_map=False):
+        prns = [int(p) for p in prns]
+        res = acquire_all(buf, prns, cfg)
+        cases.append(dict(name=name, kind=kind, spec=spec, fs=buf.sample_rate_hz,
+                          n_samples=len(buf), input_sha256=sha(buf.samples), prns=prns,
+                          config=cfg_dict(cfg), results=[res_dict(r) for r in res]))
+        if keep_map:
+            for p in keep_map:
+                maps[f"{name}__prn{p}"] = ref_power_map(buf, p, cfg)
+        print(f"{name}: {len(prns)} prns  ({time.time() - t0:.1f}s)", flush=True)
+
+    all_prns = list(range(1, 33))
+    g2 = AcqConfig(doppler_min_hz=-5000.0, doppler_max_hz=5000.0, doppler_step_hz=500.0,
+                   noncoherent_rounds=2)
+    for fs, tag in ((5.0e6, "5M"), (2.5e6, "2M5"), (8.192e6, "8M192"), (3.0e6, "3M")):
+        for i in range(2):
+            buf, truth = ref_snapshot(i, fs, 2e-3, base_seed=900)
+            add(f"gen{tag}_snap{i}", "snapshot", dict(index=i, fs=fs, duration_s=2e-3, base_seed=900,
+                                                     truth=truth), buf, all_prns, g2,
+                keep_map=([truth[0][0], 5] if i == 0 and fs == 5.0e6 else False))
+    # 2 ms coherent (n_coh = 2 P), 6 MHz; and a 10 ms C3-style search at 5 MHz
+    buf, truth = ref_snapshot(0, 6.0e6, 4e-3, base_seed=910)
+    add("gen6M_coh2", "snapshot", dict(index=0, fs=6.0e6, duration_s=4e-3, base_seed=910, truth=truth),
+        buf, all_prns, AcqConfig(coherent_ms=2, noncoherent_rounds=2, doppler_step_hz=250.0),
+        keep_map=[truth[0][0]])
+    buf, truth = ref_snapshot(1, 5.0e6, 10e-3, base_seed=920)
+    add("gen5M_c3", "snapshot", dict(index=1, fs=5.0e6, duration_s=10e-3, base_seed=920, truth=truth),
+        buf, all_prns, C3)
+    nb = noise_buffer(3, round(5.0e6 * 2e-3), 5.0e6)
+    add("gen5M_noise", "noise", dict(seed=3, n=len(nb), fs=5.0e6), nb, [1, 7, 30], g2)
+    s = dict(prn=12, doppler_hz=-1750.0, code_phase_samples=2345.0, carrier_phase_cycles=0.25,
+             fs=5.0e6, duration_s=2e-3, noise_sigma=0.0, seed=0)
+    b = synthesize_signal(SignalSpec(prn=12, doppler_hz=-1750.0, code_phase_samples=2345.0,
+                                     carrier_phase_cycles=0.25, sample_rate_hz=5.0e6, duration_s=2e-3))
+    add("gen5M_truth", "synth", s, b, [12, 13], g2)
+    (OUT / "golden_generic.json").write_text(json.dumps(dict(
+        generator="tests/golden/make_golden.py --generic", reference="gnssperf 0.1.0 (/root/reference/pkg)",
+        numpy=np.__version__, scipy=__import__("scipy").__version__, cases=cases), indent=1))
+    np.savez_compressed(OUT / "maps_generic.npz", **maps)
+    print("wrote", len(cases), "generic cases,", len(maps), "maps in", round(time.time() - t0, 1), "s")
 
 
 if __name__ == "__main__":

@@ -91,10 +91,14 @@ def test_buffer_validation_order_and_messages(pkg):
         pkg.acquire_channel(dbl, pkg.CaCode(1, oracle.generate_ca_code(1)), cfg)
 
 
-def test_create_rejects_unaligned_sample_rate_before_touching_a_device(pkg):
-    # 5 MHz is a valid reference rate but not chip-aligned: refused loudly, never a CPU path
-    with pytest.raises(pkg.UnsupportedError, match="D\\*1.023 MHz"):
-        pkg.AcqEngine(5e6, [1], pkg.AcqConfig())
+def test_create_rejects_oversized_generic_rate_before_touching_a_device(pkg):
+    # 20 MHz is not chip-aligned and its generic transform (n_coh + P - 1 -> 65536 points)
+    # exceeds the two-CTA limit: refused loudly, never a CPU path
+    with pytest.raises(pkg.UnsupportedError, match="generic path"):
+        pkg.AcqEngine(20e6, [1], pkg.AcqConfig())
+    # 8.192 MHz with 4 ms coherent: 32768 + 8192 - 1 points -> 65536, also refused
+    with pytest.raises(pkg.UnsupportedError, match="generic path"):
+        pkg.AcqEngine(8.192e6, [1], pkg.AcqConfig(coherent_ms=4))
 
 
 def test_create_without_gpu_raises_resource_error(pkg):

@@ -225,3 +225,39 @@ def test_plans_with_different_rates_coexist(pkg):
         assert rows.shape == (1, 2)
     for eng in engines:
         eng.close()
+
+
+GENERIC_ON_ALIGNED = ["c1_snap0", "c1_snap1", "c3_snap0", "coh2_snap0", "fs8_snap0", "radius10_snap1",
+                      "direct_full_2046k", "zeros_c1", "noise_seed0", "ka_prn5_1500_4000",
+                      "c4_snap0"]  # 16.368 MHz: M = 32768, the two-part (L = 2) transform
+
+
+@pytest.mark.parametrize("name", GENERIC_ON_ALIGNED)
+def test_generic_path_on_chip_aligned_cases(pkg, name, monkeypatch):
+    # the power-of-two path (gacq_generic.cuh) that serves rates which are not chip-aligned,
+    # forced onto chip-aligned golden cases: same reference answers as the 1023-point path
+    monkeypatch.setenv("GACQ_PATH", "generic")
+    c = case(name)
+    eng = pkg.AcqEngine(c["fs"], c["prns"], to_cfg(pkg, c))
+    assert eng.info["path"] == 4 and eng.info["fft_len"] >= eng.info["n_coh"] + eng.info["samples_per_period"] - 1
+    res = eng.search(case_input(c)).results()[0]
+    cfg = oracle_config(c)
+    for g, r in zip(res, c["results"]):
+        gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples, peak_metric=g.peak_metric,
+                  detected=g.detected)
+        verdict = compare(gd, r, c["config"]["detection_threshold"])
+        if verdict not in ("exact", "tie"):
+            pmap = oracle.acquire_channel(case_input(c), c["fs"], r["prn"], cfg, want_map=True)["power_map"]
+            verdict = compare(gd, r, c["config"]["detection_threshold"], pmap, cfg.doppler_bins_hz())
+        assert verdict in ("exact", "tie"), f"{name} prn {r['prn']}: {verdict}"
+    eng.close()
+
+
+def test_generic_rates_use_the_generic_path(pkg):
+    for fs in (5.0e6, 2.5e6, 8.192e6, 3.0e6, 6.0e6):
+        eng = pkg.AcqEngine(fs, [1], pkg.AcqConfig(noncoherent_rounds=1))
+        assert eng.info["path"] == 4, (fs, eng.info)
+        eng.close()
+    eng = pkg.AcqEngine(4.092e6, [1], pkg.AcqConfig(noncoherent_rounds=1))
+    assert eng.info["path"] == 2
+    eng.close()
