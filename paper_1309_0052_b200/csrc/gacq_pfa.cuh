@@ -193,7 +193,7 @@ template <bool kRegs>
 __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
     __shared__ float red_v[kCorrMaxWarps], red_f[kCorrMaxWarps];
     __shared__ int red_i[kCorrMaxWarps];
-    __shared__ long long s_claim;
+    __shared__ long long s_claim, s_claim0;  // s_claim0: the first claim (read before the item loop)
     __shared__ float s_coef[15][32];  // coop31 columns, read conflict-free as s_coef[j-1][lane]
     extern __shared__ __align__(16) cx smem[];
     const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -213,7 +213,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(ccs + 2 * i, g + 16 * i);
         cp_async_commit();
     };
-    if (threadIdx.x == 0) s_claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
+    if (threadIdx.x == 0) s_claim0 = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
     load_cc(item);
 
     const int rho0 = w * a.PW;
@@ -227,7 +227,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     const int pl = lane == 0 ? 0 : 31 - lane;  // Hermitian partner column of k1 = lane
     cp_async_wait_all();
     __syncthreads();
-    int64_t next = s_claim;
+    int64_t next = s_claim0;  // s_claim itself is rewritten by thread 0 at the end of the first item
 
     for (;;) {
         long long claim = 0;

@@ -37,7 +37,7 @@ template <bool kRegs>
 __global__ void __launch_bounds__(32 * kTcWarps, 3) gacq_corr_tc_kernel(CorrPfaArgs a, const float4* __restrict__ tcB) {
     __shared__ float red_v[kTcWarps], red_f[kTcWarps];
     __shared__ int red_i[kTcWarps];
-    __shared__ long long s_claim;
+    __shared__ long long s_claim, s_claim0;  // s_claim0: the first claim (read before the item loop)
     __shared__ float s_coef[15][32];
     __shared__ uint32_t s_tmem;
     __shared__ __align__(8) unsigned long long s_mma_bar;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, 3) gacq_corr_tc_kernel(CorrPfaA
         for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(ccs + 2 * i, g + 16 * i);
         cp_async_commit();
     };
-    if (threadIdx.x == 0) s_claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
+    if (threadIdx.x == 0) s_claim0 = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
     load_cc(item);
     const int rho0 = w * a.PW;
     const int nph = a.PW;
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, 3) gacq_corr_tc_kernel(CorrPfaA
     const int pl = lane == 0 ? 0 : 31 - lane;
     cp_async_wait_all();
     __syncthreads();
-    int64_t next = s_claim;
+    int64_t next = s_claim0;  // s_claim itself is rewritten by thread 0 at the end of the first item
 
     for (;;) {
         long long claim = 0;
