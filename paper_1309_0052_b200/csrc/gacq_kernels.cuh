@@ -164,12 +164,16 @@ __device__ __forceinline__ void wipe_fold(const cx* __restrict__ x, const cx* __
         const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x);
         const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(c);
         const int np = P / 2;
-        for (int base = threadIdx.x; base < np; base += 4 * NT) {
-            cx w[4][2];
+#ifndef GACQ_WIPE_U
+#define GACQ_WIPE_U 4
+#endif
+        constexpr int U = GACQ_WIPE_U;  // 16-byte load pairs in flight per thread
+        for (int base = threadIdx.x; base < np; base += U * NT) {
+            cx w[U][2];
             for (int k = 0; k < K; ++k) {
-                ulonglong2 xv[4], cv[4];
+                ulonglong2 xv[U], cv[U];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const int i = base + u * NT;
                     if (i < np) {
                         xv[u] = __ldg(x2 + k * np + i);
@@ -177,14 +181,14 @@ __device__ __forceinline__ void wipe_fold(const cx* __restrict__ x, const cx* __
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < U; ++u) {
                     const cx p0 = cmul_exact(xv[u].x, cv[u].x), p1 = cmul_exact(xv[u].y, cv[u].y);
                     w[u][0] = k ? add2(w[u][0], p0) : p0;
                     w[u][1] = k ? add2(w[u][1], p1) : p1;
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int i = base + u * NT;
                 if (i < np) {
                     put(2 * i, w[u][0]);

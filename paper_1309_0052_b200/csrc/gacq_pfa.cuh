@@ -32,7 +32,13 @@ constexpr int kCcHalf = 17 * 32;                 // Hermitian half of a conj cod
 #endif
 
 __host__ __device__ constexpr int corr_pfa_smem(int W) { return W * (kCorrWarpCx * 8 + 16) + kCcHalf * 8; }
-__host__ __device__ constexpr int fwd_pfa_smem(int D, int W) { return 8 * (D * fwd_ws(D) + W * (kBuf + kScr)); }
+// K1 with one phase per warp (W == D) computes every chip sum before any warp writes its
+// exchange tile, so the exchange tiles alias the wiped-block table (one barrier in between)
+__host__ __device__ constexpr bool fwd_pfa_alias(int D, int W) { return W == D; }
+__host__ __device__ constexpr int fwd_pfa_smem(int D, int W) {
+    return fwd_pfa_alias(D, W) ? 8 * (D * fwd_ws(D) > W * (kBuf + kScr) ? D * fwd_ws(D) : W * (kBuf + kScr))
+                               : 8 * (D * fwd_ws(D) + W * (kBuf + kScr));
+}
 
 // ---- bulk async copy + mbarrier (SASS UBLKCP / SYNCS) ------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -66,6 +72,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ float pow_acc(cx v, float acc) { return fmaf(im(v), im(v), fmaf(re(v), re(v), acc)); }
 
 // ---- K1 ---------------------------------------------------------------------------------
+#ifndef GACQ_FWD_MINB
+#define GACQ_FWD_MINB(W) (16 / (W) > 0 ? 16 / (W) : 1)  // <= 128 registers: 16 warps per SM
+#endif
 struct FwdPfaArgs {
     const float2* snaps;   // batch base (device), snapshot s at snaps + s*stride
     int64_t stride;        // complex samples between snapshots
@@ -79,7 +88,7 @@ struct FwdPfaArgs {
 // phases rho in [w PWF, (w+1) PWF), PWF = ceil(D/W), sliding the chip sums by one sample per
 // phase. dynamic smem: fwd_pfa_smem(D, W).
 template <int D, int W>
-__global__ void __launch_bounds__(32 * W) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
+__global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(W)) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
     constexpr int WS = fwd_ws(D);
     constexpr int PWF = (D + W - 1) / W;
     extern __shared__ __align__(16) cx smem[];
@@ -92,7 +101,8 @@ __global__ void __launch_bounds__(32 * W) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
                          reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh, a.P, a.K, wt);
 
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    cx* T = smem + D * WS + w * (kBuf + kScr);  // exchange [k1][33]
+    constexpr bool kAlias = fwd_pfa_alias(D, W);
+    cx* T = smem + (kAlias ? 0 : D * WS) + w * (kBuf + kScr);  // exchange [k1][33]
     cx* scr = T + kBuf;
     float coef[15];
 #pragma unroll
@@ -123,6 +133,7 @@ __global__ void __launch_bounds__(32 * W) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
                 zr[n1] = chip_sum(rho, m);
             }
             ze = lane < 31 ? chip_sum(rho, me) : czero();
+            if (kAlias) __syncthreads();  // every warp's chip sums are read before T overwrites wt
         } else {  // window [rho-1, rho-1+D) -> [rho, rho+D): drop wbar[D m + rho-1], add wbar[D (m+1) + rho-1]
             const cx* r = wt + (rho - 1) * WS;
 #pragma unroll
