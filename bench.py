@@ -186,38 +186,19 @@ class ClockSampler:
 
 
 def synth_batch(torch, n, c, seed, device):
-    """Synthetic GPS-like snapshots on the GPU: 8 visible satellites (random PRN, Doppler
-    U(-4750,4750), integer code phase, carrier phase, C/N0 U(38,48) dB-Hz) + AWGN at the
-    45 dB-Hz reference level. Perf input only (parity uses the oracle's synthesis)."""
-    from paper_1309_0052_b200 import generate_ca_code
+    """Synthetic GPS snapshots generated in HBM by libgacq (gacq_synth):
+    8 visible satellites per snapshot (distinct PRNs, Doppler U(-span+250, span-250), integer
+    code phase, carrier phase, C/N0 U(38,48) dB-Hz) + AWGN at the 45 dB-Hz reference level.
+    Perf input only (parity uses the oracle's synthesis of the reference's PCG64 stream)."""
+    import paper_1309_0052_b200 as g
 
     fs = c["fs"]
     span = round(fs * 1e-3) * c["rounds"]
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    chips = torch.tensor(np.stack([generate_ca_code(p).chips for p in range(1, 33)]),
-                         dtype=torch.float32, device=device)
+    sats = g.random_sats(np.random.default_rng(seed), n, fs, doppler_span_hz=c["span_hz"] - 250.0)
     out = torch.empty((n, span), dtype=torch.complex64, device=device)
-    idx = torch.arange(span, device=device, dtype=torch.int64)
     sigma = math.sqrt(fs / (2.0 * 10.0 ** (45.0 / 10.0)))
-    chunk = 32
-    for s0 in range(0, n, chunk):
-        m = min(chunk, n - s0)
-        noise = torch.randn((m, span, 2), generator=g, device=device) * sigma
-        x = torch.view_as_complex(noise.contiguous())
-        for _ in range(8):
-            prn = torch.randint(0, 32, (m,), generator=g, device=device)
-            dop = (torch.rand((m,), generator=g, device=device, dtype=torch.float64) * 2 - 1) * (c["span_hz"] - 250)
-            cph = torch.randint(0, round(fs * 1e-3), (m,), generator=g, device=device)
-            carr = torch.rand((m,), generator=g, device=device, dtype=torch.float64)
-            cn0 = 38.0 + 10.0 * torch.rand((m,), generator=g, device=device, dtype=torch.float64)
-            amp = (10.0 ** ((cn0 - 45.0) / 20.0)).to(torch.float32)
-            ci = torch.div((idx[None, :] - cph[:, None]) * 1023000, round(fs), rounding_mode="floor").remainder(1023)
-            code = chips[prn[:, None], ci]
-            ph = torch.frac(dop[:, None] * idx[None, :].double() / fs + carr[:, None]) * (2 * math.pi)
-            x += (amp[:, None] * code) * torch.polar(torch.ones_like(ph, dtype=torch.float32), ph.float())
-        out[s0:s0 + m] = x
-    return out
+    return g.synthesize_batch(sats, fs, span, out, noise_sigma=sigma, seed=seed,
+                              device=device.index if device.index is not None else 0)
 
 
 # ------------------------------------------------------------------ arms
@@ -415,7 +396,7 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic (8 satellites + AWGN per snapshot, generated on device)",
+        "data": "synthetic (8 satellites + AWGN per snapshot, generated in HBM by gacq_synth)",
         "config": {"workload": c["desc"], "snapshots_per_gpu": batch, "global_batch": batch * world,
                    "cells_per_step_per_gpu": cells_step, "fs_hz": c["fs"], "prns": 32, "bins": n_bins,
                    "parallelism": f"dp{world} (snapshot shards, no collective)",

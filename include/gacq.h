@@ -140,6 +140,27 @@ int gacq_power_map(gacq_ctx* ctx, const void* snap_host, float* out_host);
  * (gnss_signal.py:49-72 -> kernels.py:106-114) for every bin f. */
 int gacq_carrier_table(gacq_ctx* ctx, void* out_host);
 
+/* ---- On-device synthetic snapshots ------------------------
+ * Replaces the benchmark-input side of synthesize_signal / add_awgn (gnss_signal.py:136-186)
+ * for large batches: out[s][k] (complex64, device memory, n_snap x n_samples) = the sum, in
+ * order, of sats[s][j].amplitude * code * carrier for the n_sat satellites of snapshot s --
+ * the same fixed-point NCO words and complex64 rounding as the reference, so with
+ * noise_sigma = 0 it is bit-identical to summing synthesize_signal(...) * float32(amp) -- plus
+ * complex AWGN of std noise_sigma per component from a counter-based Philox stream (the
+ * reference's PCG64 stream is not reproduced: performance inputs only, never parity). */
+typedef struct gacq_sat {
+    int32_t prn;                 /* 1..32 (SignalSpec.prn)                     */
+    int32_t reserved;
+    double doppler_hz;           /* SignalSpec.doppler_hz                      */
+    double code_phase_samples;   /* SignalSpec.code_phase_samples, [0, P)      */
+    double carrier_phase_cycles; /* SignalSpec.carrier_phase_cycles            */
+    float amplitude;             /* float32 scale applied to the clean signal  */
+    float reserved2;
+} gacq_sat;
+
+int gacq_synth(int32_t device, double sample_rate_hz, int64_t n_snap, int64_t n_samples, int32_t n_sat,
+               const gacq_sat* sats_host, double noise_sigma, uint64_t seed, void* out_device);
+
 int gacq_stats_get(const gacq_ctx* ctx, gacq_stats* out);
 int gacq_stats_reset(gacq_ctx* ctx);
 

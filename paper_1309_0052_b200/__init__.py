@@ -19,6 +19,7 @@ from .acquisition import (  # noqa: F401
     samples_per_code_period,
 )
 from .buffers import IqBuffer, Precision  # noqa: F401
+from .synth import SAT_DTYPE, random_sats, synthesize_batch  # noqa: F401
 from .iffile import IfPayload, read_if_file, read_if_payload, write_if_file  # noqa: F401
 from .cacode import CHIP_RATE_HZ, CODE_LENGTH, CaCode, generate_ca_code  # noqa: F401
 from .errors import (  # noqa: F401

@@ -33,6 +33,12 @@ class Info(C.Structure):
                                          "n_bins", "n_prn", "rounds", "path", "corr_ctas")]
 
 
+class Sat(C.Structure):
+    _fields_ = [("prn", C.c_int32), ("reserved", C.c_int32), ("doppler_hz", C.c_double),
+                ("code_phase_samples", C.c_double), ("carrier_phase_cycles", C.c_double),
+                ("amplitude", C.c_float), ("reserved2", C.c_float)]
+
+
 class Stats(C.Structure):
     _fields_ = [("calls", C.c_int64), ("launches", C.c_int64), ("cells", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("fwd_ms", C.c_double),
@@ -46,7 +52,7 @@ ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
 EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
            "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
            "gacq_host_alloc", "gacq_host_free", "gacq_ca_code", "gacq_trk_create", "gacq_trk_destroy",
-           "gacq_trk_epl", "gacq_carrier_table")
+           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth")
 FMT_INT8, FMT_INT16 = 0, 1
 
 
@@ -66,6 +72,8 @@ def _load() -> C.CDLL:
                                        C.c_uint32, C.c_void_p]
     lib.gacq_power_map.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.gacq_carrier_table.argtypes = [C.c_void_p, C.c_void_p]
+    lib.gacq_synth.argtypes = [C.c_int32, C.c_double, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_double,
+                               C.c_uint64, C.c_void_p]
     lib.gacq_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]
     lib.gacq_stats_reset.argtypes = [C.c_void_p]
     lib.gacq_host_alloc.argtypes = [C.c_int64, C.POINTER(C.c_void_p)]

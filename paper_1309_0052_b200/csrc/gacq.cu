@@ -886,6 +886,70 @@ int gacq_carrier_table(gacq_ctx* c, void* out) {
     return GACQ_OK;
 }
 
+int gacq_synth(int32_t device, double fs, int64_t n_snap, int64_t n, int32_t n_sat, const gacq_sat* sats,
+               double sigma, uint64_t seed, void* out) {
+    if (!out || (n_sat > 0 && !sats)) return fail(GACQ_ERR_INVALID, "null argument");
+    if (!(fs > 0) || !std::isfinite(fs) || n_snap < 1 || n < 1 || n_sat < 0)
+        return fail(GACQ_ERR_INVALID, "sample rate, n_snap and n_samples must be > 0");
+    if (!(sigma >= 0) || !std::isfinite(sigma)) return fail(GACQ_ERR_INVALID, "noise_sigma must be >= 0");
+    auto pymod = [](double a, double m) {  // Python's float a % m for m > 0
+        double r = std::fmod(a, m);
+        if (r != 0 && r < 0) r += m;
+        return r;
+    };
+    const double cps = kChipRate / fs;
+    std::vector<SynthSat> st((size_t)n_snap * n_sat);
+    for (size_t i = 0; i < st.size(); ++i) {
+        const gacq_sat& g = sats[i];
+        if (g.prn < 1 || g.prn > 32) return fail(GACQ_ERR_INVALID, "prn must be in 1..32");
+        const double code0 = pymod(-g.code_phase_samples * cps, 1023.0);  // gnss_signal.py:170-171
+        st[i].code_p0 = (uint64_t)py_mod(py_round(pymod(code0, 1023.0) * (double)kCodeScale), kCodeModulus);
+        const double carr0 = pymod(-g.carrier_phase_cycles, 1.0);          // gnss_signal.py:180
+        st[i].carrier_p0 = (uint64_t)py_mod(py_round(pymod(carr0, 1.0) * (double)kCarrierScale), kCarrierScale);
+        st[i].carrier_step = (uint64_t)py_mod(py_round((-g.doppler_hz / fs) * (double)kCarrierScale), kCarrierScale);
+        st[i].prn_index = g.prn - 1;
+        st[i].amp = g.amplitude;
+    }
+    const uint64_t code_step = (uint64_t)py_round(cps * (double)kCodeScale);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(GACQ_ERR_CUDA, "no CUDA device visible");
+    }
+    if (device < 0 || device >= ndev) return fail(GACQ_ERR_INVALID, "device %d out of range", device);
+    DeviceGuard g(device);
+    SynthSat* d_st = nullptr;
+    int32_t* d_prns = nullptr;
+    int8_t* d_chips = nullptr;
+    cudaStream_t stream = nullptr;
+    auto work = [&]() -> cudaError_t {
+        cudaError_t e;
+        std::vector<int32_t> all(32);
+        for (int i = 0; i < 32; ++i) all[i] = i + 1;
+        if ((e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking)) ||
+            (e = cudaMalloc(&d_st, std::max<size_t>(1, st.size()) * sizeof(SynthSat))) ||
+            (e = cudaMalloc(&d_prns, 32 * sizeof(int32_t))) || (e = cudaMalloc(&d_chips, 32 * kChips)))
+            return e;
+        if ((!st.empty() &&
+             (e = cudaMemcpyAsync(d_st, st.data(), st.size() * sizeof(SynthSat), cudaMemcpyHostToDevice, stream))) ||
+            (e = cudaMemcpyAsync(d_prns, all.data(), 32 * sizeof(int32_t), cudaMemcpyHostToDevice, stream)))
+            return e;
+        gacq_ca_chips_kernel<<<1, 32, 0, stream>>>(d_prns, 32, d_chips);
+        const int64_t total = n_snap * n;
+        gacq_synth_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, stream>>>(
+            d_st, n_sat, n_snap, n, code_step, d_chips, kTwoPi / (double)kCarrierScale, sigma, seed, (float2*)out);
+        if ((e = cudaGetLastError())) return e;
+        return cudaStreamSynchronize(stream);
+    };
+    const cudaError_t e = work();
+    cudaFree(d_st);
+    cudaFree(d_prns);
+    cudaFree(d_chips);
+    if (stream) cudaStreamDestroy(stream);
+    if (e != cudaSuccess) return fail(GACQ_ERR_CUDA, "gacq_synth failed: %s", cudaGetErrorString(e));
+    return GACQ_OK;
+}
+
 int gacq_host_alloc(int64_t bytes, void** out) {
     if (!out || bytes <= 0) return fail(GACQ_ERR_INVALID, "bad host allocation request");
     if (cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) {

@@ -79,3 +79,67 @@ __global__ void gacq_code_spectrum_kernel(const int8_t* __restrict__ chips, int 
 }
 
 }  // namespace gacq
+
+namespace gacq {
+
+// ---- on-device synthetic snapshots (perf inputs, never parity) ----
+// One satellite of one snapshot with the reference's fixed-point NCO words (gnss_signal.py:157-186
+// with kernels.py:56-70): code_p0 = code_phase_to_fixed((-code_phase * 1.023e6/fs) mod 1023),
+// carrier_p0 = carrier_phase_to_fixed((-carrier_phase) mod 1), carrier_step for -doppler.
+struct SynthSat {
+    uint64_t code_p0, carrier_p0, carrier_step;
+    int32_t prn_index;  // 0..31
+    float amp;          // float32 scale (10^((cn0 - cn0_ref)/20))
+};
+
+// Philox4x32-10 (counter-based; the reference's PCG64 stream is not reproduced)
+__device__ __forceinline__ uint4 philox(uint4 ctr, uint2 key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const unsigned hi0 = __umulhi(0xD2511F53u, ctr.x), lo0 = 0xD2511F53u * ctr.x;
+        const unsigned hi1 = __umulhi(0xCD9E8D57u, ctr.z), lo1 = 0xCD9E8D57u * ctr.z;
+        ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+        key.x += 0x9E3779B9u;
+        key.y += 0xBB67AE85u;
+    }
+    return ctr;
+}
+
+// out[s][k] = sum over the snapshot's satellites, in order, of amp * code(k) * carrier(k)
+// (complex64, as the reference sums them), plus sigma * (N(0,1) + i N(0,1)) rounded to complex64
+// when sigma > 0 (Box-Muller in float64 on Philox uniforms, gnss_signal.py:136-154).
+__global__ void gacq_synth_kernel(const SynthSat* __restrict__ sats, int n_sat, int64_t n_snap, int64_t n,
+                                  uint64_t code_step, const int8_t* __restrict__ chips, double inv, double sigma,
+                                  uint64_t seed, float2* __restrict__ out) {
+    const int64_t total = n_snap * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / n;
+        const uint64_t k = (uint64_t)(i - s * n);
+        float re = 0.f, im = 0.f;
+        for (int j = 0; j < n_sat; ++j) {
+            const SynthSat st = sats[s * n_sat + j];
+            const uint64_t cph = (st.code_p0 + k * code_step) % (1023ull << 42);
+            const float chip = (float)chips[st.prn_index * kChips + (int)(cph >> 42)];
+            const uint64_t ph = (st.carrier_p0 + k * st.carrier_step) & ((1ull << 48) - 1);
+            double sn, cs;
+            sincos(__dmul_rn((double)ph, inv), &sn, &cs);
+            // code (+-1, 0) x carrier (cos, -sin): exact; then x amp; summed in draw order
+            re = __fadd_rn(re, __fmul_rn(chip * (float)cs, st.amp));
+            im = __fadd_rn(im, __fmul_rn(chip * (float)(-sn), st.amp));
+        }
+        if (sigma > 0.0) {
+            const uint4 r = philox(make_uint4((unsigned)i, (unsigned)(i >> 32), 0x5851F42Du, 0x14057B7Eu),
+                                   make_uint2((unsigned)seed, (unsigned)(seed >> 32)));
+            const double u1 = 1.0 - ((double)(((uint64_t)r.x << 21) ^ r.y) * 0x1p-53);  // (0, 1]
+            const double u2 = (double)(((uint64_t)r.z << 21) ^ r.w) * 0x1p-53;
+            const double rad = sqrt(-2.0 * log(u1));
+            double s2, c2;
+            sincospi(2.0 * u2, &s2, &c2);
+            re = __fadd_rn(re, (float)(sigma * (rad * c2)));
+            im = __fadd_rn(im, (float)(sigma * (rad * s2)));
+        }
+        out[i] = make_float2(re, im);
+    }
+}
+
+}  // namespace gacq
