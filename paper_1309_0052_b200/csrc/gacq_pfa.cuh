@@ -327,13 +327,33 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 f(accx[0], a.D * cell_q(0, 32) + rho0);
             }
         };
-        if (kRegs) for_cells([&](float v, int lag) { if (better(v, lag, best, bidx)) { best = v; bidx = lag; } });
         // first argmax of the item (acquisition.py:151): ties -> lowest lag
+        const bool x0 = lane >= 1 && lane <= 16, x1 = lane >= 1 && lane <= 15;  // lanes owning coop cells
+        float lane_max = 0.f;
+        if (kRegs) {
+            // warp max of the values, then the lowest lag holding it (searched only by the lanes
+            // whose own max equals it). Lanes without coop cells keep accx = 0, which is <= every
+            // power and never a lag candidate.
+            float m = acc[0];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, best, off);
-            const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
-            if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
+            for (int q1 = 1; q1 < 31; ++q1) m = fmaxf(m, acc[q1]);
+            m = fmaxf(m, fmaxf(accx[0], accx[1]));
+            lane_max = m;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+            int bl = 0x7fffffff;
+            if (lane_max == m) for_cells([&](float v, int lag) { if (v == m && lag < bl) bl = lag; });
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) bl = min(bl, __shfl_xor_sync(0xffffffffu, bl, off));
+            best = m;
+            bidx = bl;
+        } else {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+                if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
+            }
         }
         if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
         if (threadIdx.x == 0) s_claim = claim;
@@ -351,7 +371,37 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         const int b = (int)(pair % a.B);
         float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
         float fl = -1.f;
-        if (kRegs) {
+        if (kRegs && !pm) {
+            // Only the cells within `radius` of the peak are excluded: lags D q + rho0 for q in
+            // [ceil((peak - r - rho0)/D), floor((peak + r - rho0)/D)] (mod 1023), at most 2r/D + 1
+            // of them. Cell q lives at (q1, q2) = (16 q mod 31, 16 q mod 33) (inverse of cell_q).
+            // A lane with none of them takes its plain max.
+            if (2 * a.radius + 1 < a.P) {
+                const int lo = peak - a.radius - rho0, hi = peak + a.radius - rho0;
+                const int qa = lo >= 0 ? (lo + a.D - 1) / a.D : -(-lo / a.D);
+                const int qb = hi >= 0 ? hi / a.D : -((-hi + a.D - 1) / a.D);
+                unsigned m31 = 0u, mx = 0u;
+                for (int q = qa; q <= qb; ++q) {
+                    const int qq = q < 0 ? q + kChips : q >= kChips ? q - kChips : q;
+                    const int q1 = (16 * qq) % 31, q2 = (16 * qq) % 33;
+                    if (q2 == lane) m31 |= 1u << q1;
+                    if (q2 == 32) {
+                        if (lane == 16 && q1 == 0) mx |= 1u;
+                        if (x1 && q1 == lane) mx |= 1u;
+                        if (x1 && q1 == 31 - lane) mx |= 2u;
+                    }
+                }
+                if ((m31 | mx) == 0u) {
+                    fl = lane_max;  // the fake 0 of lanes without coop cells never raises the floor
+                } else {
+#pragma unroll
+                    for (int q1 = 0; q1 < 31; ++q1)
+                        if (!((m31 >> q1) & 1u)) fl = fmaxf(fl, acc[q1]);
+                    if (x0 && !(mx & 1u)) fl = fmaxf(fl, accx[0]);
+                    if (x1 && !(mx & 2u)) fl = fmaxf(fl, accx[1]);
+                }
+            }
+        } else if (kRegs) {
             for_cells([&](float v, int lag) {
                 if (!excluded(lag, peak, a.P, a.radius)) fl = fmaxf(fl, v);
                 if (pm) pm[lag] = v;
