@@ -104,9 +104,6 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(W)) gacq_fwd_pfa_kernel(
     constexpr bool kAlias = fwd_pfa_alias(D, W);
     cx* T = smem + (kAlias ? 0 : D * WS) + w * (kBuf + kScr);  // exchange [k1][33]
     cx* scr = T + kBuf;
-    float coef[15];
-#pragma unroll
-    for (int j = 1; j <= 15; ++j) coef[j - 1] = coop31_coef(lane, j);
     // lane n2 holds z at m = (33 n1 + 31 n2) mod 1023, n1 < 31; lane L < 31 also holds row
     // n2 = 32 at m = (33 L + 992) mod 1023
     const int mb = 31 * lane, me = (33 * lane + 992) % kChips;
@@ -150,7 +147,7 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(W)) gacq_fwd_pfa_kernel(
 #pragma unroll
             for (int n1 = 0; n1 < 31; ++n1) x[n1] = zr[n1];
             dft_odd<-1, 31, 5>(x, [&](int k1, cx v) { T[k1 * 33 + lane] = v; });
-            coop31<-1>(ze, lane, [&](int j) { return coef[j - 1]; }, scr,
+            coop31<-1>(ze, lane, [&](int j) { return __ldg(&kCoop31Coef[j - 1][lane]); }, scr,
                        [&](int, int k1, cx v) { T[k1 * 33 + 32] = v; });
         }
         __syncwarp();
