@@ -18,6 +18,7 @@
 #pragma once
 #include "gacq_kernels.cuh"
 #include "pfa.cuh"
+#include "rader31.cuh"
 
 namespace gacq {
 
@@ -27,6 +28,9 @@ constexpr unsigned kSpecBytes = kBuf * sizeof(cx);
 constexpr int kCorrMaxWarps = 6;
 constexpr int kCorrWarpCx = 2 * kBuf;            // per-warp shared memory (cx): two spectra
 constexpr int kCcHalf = 17 * 32;                 // Hermitian half of a conj code spectrum (cx)
+#ifndef GACQ_RADER31
+#define GACQ_RADER31 1                           // K2's 31-point stage by Rader's algorithm (rader31.cuh)
+#endif
 #ifndef GACQ_PFA_MAXNREG
 #define GACQ_PFA_MAXNREG 168                     // 3 CTAs x 4 warps per SM; no spills (streamed stages)
 #endif
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(W)) gacq_fwd_pfa_kernel(
             cx x[31];
 #pragma unroll
             for (int n1 = 0; n1 < 31; ++n1) x[n1] = zr[n1];
-            dft_odd<-1, 31, 5>(x, [&](int k1, cx v) { T[k1 * 33 + lane] = v; });
+            dft_odd<-1, 31, 5>(x, [&](int k1, cx v) { T[k1 * 33 + lane] = v; });  // (Rader measured slower here)
             coop31<-1>(ze, lane, [&](int j) { return __ldg(&kCoop31Coef[j - 1][lane]); }, scr,
                        [&](int, int k1, cx v) { T[k1 * 33 + 32] = v; });
         }
@@ -284,8 +288,12 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
             // scratch in the buffer's unused tail E[1023..1055])
             const cx e = lane < 31 ? E[32 * 31 + lane] : czero();
             const cx* Er = E + lane * 31;
+#if GACQ_RADER31
+            dft31_rader_inv([&](int k1) { return Er[k1]; }, [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+#else
             dft31_stream<1>([&](int k1, int dep) { return Er[k1 + dep]; }, a.zero,
                             [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+#endif
             coop31<1>(e, lane, [&](int j) { return s_coef[j - 1][lane]; }, E + kChips,
                       [&](int sl, int, cx v) { accx[sl] = pow_acc(v, accx[sl]); });
             __syncwarp();  // E is free for the prefetch issued at the next transform
