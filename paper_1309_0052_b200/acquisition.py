@@ -342,7 +342,9 @@ def get_engine(sample_rate_hz: float, prns, config: AcqConfig, device: int = 0) 
     with _engines_lock:
         _engines[key] = eng
         while len(_engines) > _MAX_ENGINES:
-            _engines.popitem(last=False)[1].close()
+            # drop the cache's reference only: an engine another thread is still searching with
+            # stays alive until that call returns, then __del__ releases its device plan
+            _engines.popitem(last=False)
     return eng
 
 
