@@ -374,7 +374,8 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         GenArgs ga{in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
                    pmap, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
         const int gen_l = c->logM > kGenMaxLogM ? 2 : 1;
-        const int gen_smem = ((int)sizeof(float2) << c->logM) / gen_l;
+        const int gen_pts = (1 << c->logM) / gen_l;
+        const int gen_smem = (int)sizeof(float2) * (GACQ_GEN_STOCKHAM ? gen_pts + gen_pts / 16 : gen_pts);
         if (c->gen) {
             if (gen_l == 2)
                 gacq_gen_fwd_kernel<2><<<(unsigned)(np * c->R * 2), kGenThreads, gen_smem, c->stream>>>(ga);
@@ -722,13 +723,13 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kGenMaxM * (int)sizeof(float2)));
+                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kGenMaxM * (int)sizeof(float2)));
+                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kGenMaxM * (int)sizeof(float2)));
+                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kGenMaxM * (int)sizeof(float2)));
+                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
     }
     const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * (c->pfa ? kBuf : kM)) *
                                (int64_t)sizeof(float2);

@@ -33,7 +33,10 @@ namespace gacq {
 constexpr int kGenMaxLogM = 14;
 constexpr int kGenMaxM = 1 << kGenMaxLogM;  // points per CTA: 128 KB of complex64 in shared memory
 constexpr int kGenMaxLogMTotal = kGenMaxLogM + 1;  // M <= 2 kGenMaxM (L = 2)
-constexpr int kGenThreads = 512;
+constexpr int kGenThreads = 512;  // kGenMaxM = 32 * kGenThreads (gen_fft_stockham)
+#ifndef GACQ_GEN_STOCKHAM
+#define GACQ_GEN_STOCKHAM 1  // register-radix Stockham passes (0: in-place radix-4 DIT from bit-reversed input)
+#endif
 
 // In-place DFT of x[0, 2^logM) held in bit-reversed order, natural order out.
 // tw[e * tw_stride] = (cos, sin)(2 pi e / 2^logM), e < 2^logM / 2; S = -1 forward, +1 inverse
@@ -79,6 +82,104 @@ __device__ __forceinline__ void gen_fft_inplace(cx* __restrict__ x, int logM, co
 
 __device__ __forceinline__ int bitrev(int j, int logM) { return (int)(__brev((unsigned)j) >> (32 - logM)); }
 
+// (cos, S sin)(2 pi e / M) for any e in [0, M) from the half table (W^(e + M/2) = -W^e)
+template <int S>
+__device__ __forceinline__ cx gen_tw(const float2* __restrict__ tw, int e, int M) {
+    const bool hi = e >= (M >> 1);
+    const float2 t = __ldg(&tw[hi ? e - (M >> 1) : e]);
+    const float c = hi ? -t.x : t.x, sn = hi ? -t.y : t.y;
+    return pk(c, S < 0 ? -sn : sn);
+}
+
+template <int S, int R>
+__device__ __forceinline__ void gen_dft(cx (&v)[R]) {
+    if constexpr (R == 16) {
+        dft16<S>(v);
+    } else if constexpr (R == 8) {
+        dft8<S>(v);
+    } else if constexpr (R == 4) {
+        dft4<S>(v[0], v[1], v[2], v[3]);
+    } else {
+        const cx a = v[0];
+        v[0] = add2(a, v[1]);
+        v[1] = sub2(a, v[1]);
+    }
+}
+
+// One Stockham autosort pass of radix R over x[0, Ms) (natural order in, natural order out
+// after the last pass), in place: every thread reads and transforms its groups, the CTA
+// synchronises, then every thread writes. Group j < Ms/R reads x[j + r Ms/R], applies
+// W_(Ns R)^(S k r), k = j mod Ns, and writes x[(j / Ns) Ns R + k + r Ns]. The twiddle table
+// is the plan's W_M half table, M = L Ms (W_(Ns R)^e = W_M^(e L Ms / (Ns R))).
+// Stockham buffers are padded: element i lives at i + i/16 (the radix-16 write pattern
+// x[16 j' + r] would otherwise put a warp's 32 stores into one bank group)
+__device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
+
+template <int S, int R>
+__device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs, int logNs,
+                                                  const float2* __restrict__ tw, int L) {
+    constexpr int kGroups = 32 / R;  // 32 values per thread at Ms = 32 * blockDim
+    constexpr int kLogR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+    const int Ms = 1 << logMs, ng = Ms >> kLogR, Ns = 1 << logNs;
+    const int tw_step = L << (logMs - logNs - kLogR);  // W_(Ns R) in units of W_M
+    cx v[kGroups][R];
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+        const int j = threadIdx.x + g * blockDim.x;
+        if (j < ng) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[g][r] = x[gpad(j + r * ng)];
+            const int k = j & (Ns - 1);
+            if (logNs > 0) {
+                // W^r from the table powers W^1, W^2, W^4, W^8 and at most two products each
+                // (<= 3 roundings per twiddle): 4 loads instead of R - 1
+                const int Mt = L << logMs, e1 = k * tw_step;
+                cx w[R];
+                w[1] = gen_tw<S>(tw, e1, Mt);
+                if (R > 2) w[2] = gen_tw<S>(tw, 2 * e1, Mt);
+                if (R > 4) w[4] = gen_tw<S>(tw, 4 * e1, Mt);
+                if (R > 8) w[8] = gen_tw<S>(tw, 8 * e1, Mt);
+#pragma unroll
+                for (int r = 3; r < R; ++r) {
+                    if ((r & (r - 1)) == 0) continue;  // powers of two are loaded
+                    const int hb = r & 8 ? 8 : r & 4 ? 4 : 2;  // highest loaded power below r
+                    const int rest = r - hb;
+                    const int hb2 = rest & 4 ? 4 : rest & 2 ? 2 : 1;
+                    w[r] = rest == hb2 ? cmul(w[hb], w[rest]) : cmul(cmul(w[hb], w[hb2]), w[rest - hb2]);
+                }
+#pragma unroll
+                for (int r = 1; r < R; ++r) v[g][r] = cmul(v[g][r], w[r]);
+            }
+            gen_dft<S, R>(v[g]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+        const int j = threadIdx.x + g * blockDim.x;
+        if (j < ng) {
+            const int k = j & (Ns - 1);
+            const int d = ((j >> logNs) << (logNs + kLogR)) + k;
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[gpad(d + (r << logNs))] = v[g][r];
+        }
+    }
+    __syncthreads();
+}
+
+// In-place natural-order DFT of x[0, 2^logMs) (sign S, unnormalised): radix-16 passes, then
+// one radix-8/4/2 pass for the remaining bits. Needs 2^logMs <= 32 * blockDim.
+template <int S>
+__device__ __forceinline__ void gen_fft_stockham(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, int L) {
+    int logNs = 0;
+    for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16>(x, logMs, logNs, tw, L);
+    const int rem = logMs - logNs;
+    if (rem == 3) gen_stockham_pass<S, 8>(x, logMs, logNs, tw, L);
+    else if (rem == 2) gen_stockham_pass<S, 4>(x, logMs, logNs, tw, L);
+    else if (rem == 1) gen_stockham_pass<S, 2>(x, logMs, logNs, tw, L);
+}
+
+
 struct GenArgs {
     const float2* snaps;    // batch base (device), snapshot s at snaps + s*stride
     int64_t stride;         // complex samples between snapshots
@@ -92,18 +193,10 @@ struct GenArgs {
     int B, R, n_coh, P, logM, n_prn, radius;  // M = 2^logM in total, L = 1 or 2 CTA-sized parts
 };
 
-// (cos, S sin)(2 pi e / M) for any e in [0, M) from the half table (W^(e + M/2) = -W^e)
-template <int S>
-__device__ __forceinline__ cx gen_tw(const float2* __restrict__ tw, int e, int M) {
-    const bool hi = e >= (M >> 1);
-    const float2 t = __ldg(&tw[hi ? e - (M >> 1) : e]);
-    const float c = hi ? -t.x : t.x, sn = hi ? -t.y : t.y;
-    return pk(c, S < 0 ? -sn : sn);
-}
 
 // grid: pairs_in_chunk * R * L CTAs of kGenThreads; dynamic smem (M / L) * 8 bytes
 template <int L>
-__global__ void __launch_bounds__(kGenThreads) gacq_gen_fwd_kernel(GenArgs a) {
+__global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a) {
     extern __shared__ __align__(16) cx sm[];
     const int M = 1 << a.logM, Ms = M / L, logMs = a.logM - (L == 2), N = a.n_coh;
     const int part = blockIdx.x % L, lr = blockIdx.x / L;
@@ -119,24 +212,29 @@ __global__ void __launch_bounds__(kGenThreads) gacq_gen_fwd_kernel(GenArgs a) {
         const int n = j < N ? j : j - N;
         return cmul_exact(__ldg(&x[n]), __ldg(&c[n]));  // acquisition.py:141, kernels.py:78-86
     };
+#pragma unroll 4
     for (int j = threadIdx.x; j < Ms; j += blockDim.x) {
         cx y = wext(j);
         if (L == 2) {
             const cx u = wext(j + Ms);
             y = part == 0 ? add2(y, u) : cmul(sub2(y, u), gen_tw<-1>(a.tw, j, M));
         }
-        sm[bitrev(j, logMs)] = y;
+        sm[GACQ_GEN_STOCKHAM ? gpad(j) : bitrev(j, logMs)] = y;
     }
     __syncthreads();
+#if GACQ_GEN_STOCKHAM
+    gen_fft_stockham<-1>(sm, logMs, a.tw, L);
+#else
     gen_fft_inplace<-1>(sm, logMs, a.tw, L);
+#endif
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
-    for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[k];
+    for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[GACQ_GEN_STOCKHAM ? gpad(k) : k];
 }
 
 // grid: pairs_in_chunk * n_prn CTAs of kGenThreads (item = lp * n_prn + pi);
 // dynamic smem (M / L) * 8 bytes
 template <int L>
-__global__ void __launch_bounds__(kGenThreads) gacq_gen_corr_kernel(GenArgs a) {
+__global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a) {
     extern __shared__ __align__(16) cx sm[];
     __shared__ float red_v[kGenThreads / 32], red_f[kGenThreads / 32];
     __shared__ int red_i[kGenThreads / 32];
@@ -152,15 +250,20 @@ __global__ void __launch_bounds__(kGenThreads) gacq_gen_corr_kernel(GenArgs a) {
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M;
 #pragma unroll
         for (int part = 0; part < L; ++part) {
+#pragma unroll 8  // keep 16 L2 loads in flight per thread
             for (int k = threadIdx.x; k < Ms; k += blockDim.x)
-                sm[bitrev(k, logMs)] = cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
+                sm[GACQ_GEN_STOCKHAM ? gpad(k) : bitrev(k, logMs)] = cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
             __syncthreads();
+#if GACQ_GEN_STOCKHAM
+            gen_fft_stockham<1>(sm, logMs, a.tw, L);
+#else
             gen_fft_inplace<1>(sm, logMs, a.tw, L);
+#endif
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const int t = threadIdx.x + i * kGenThreads;
                 if (t < a.P) {
-                    cx v = sm[t];
+                    cx v = sm[GACQ_GEN_STOCKHAM ? gpad(t) : t];
                     if (L == 2 && part == 0) {
                         e0[i] = v;
                         continue;

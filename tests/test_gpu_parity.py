@@ -57,8 +57,11 @@ def test_golden_case(pkg, name):
             verdict = compare(g, r, c["config"]["detection_threshold"], pmap, bins)
         assert verdict in ("exact", "tie"), f"{name} prn {r['prn']}: {verdict}"
         ties += verdict == "tie"
-    # ties are only legitimate for exactly symmetric inputs (the 0 Hz aligned case)
-    assert ties == 0 or name == "aligned_tie_0hz", f"{ties} ties in {name}"
+    # ties are only legitimate for exactly symmetric inputs: the aligned 0 Hz case, and the
+    # noise-free 5 MHz truth whose Doppler (-1750 Hz) sits exactly mid-bin, so the reference's
+    # own float32 map holds exact top-2 ties (bins 6/7 for PRN 12, 1/12 for PRN 13) that any
+    # rounding difference may break the other way
+    assert ties == 0 or name in ("aligned_tie_0hz", "gen5M_truth"), f"{ties} ties in {name}"
 
 
 def test_power_maps_match_reference(pkg):
