@@ -328,7 +328,9 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (quantized && !inp.on_device && (rc = grow(&c->d_raw, &c->raw_cap, n_snap * span * sb))) return rc;
         in = c->d_in;
         in_stride = span;
-        copy_chunk = std::max<int64_t>(1, std::min<int64_t>(n_snap, c->z_pairs / c->B));
+        // fine-grained copies (<= 16 snapshots per event) so the first compute chunk, which is
+        // kept small below, starts after a few MB of H2D rather than after a whole chunk
+        copy_chunk = std::max<int64_t>(1, std::min<int64_t>({n_snap, c->z_pairs / c->B, (int64_t)16}));
         n_copy_chunks = (n_snap + copy_chunk - 1) / copy_chunk;
         while ((int64_t)c->copy_events.size() < n_copy_chunks) {
             cudaEvent_t e;
@@ -360,8 +362,11 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
     size_t ev = 2;
     int64_t waited = -1;
     std::vector<std::pair<size_t, int>> timed;  // (event index, kernel kind)
-    for (int64_t p0 = 0; p0 < n_pairs; p0 += c->z_pairs) {
-        const int64_t np = std::min(c->z_pairs, n_pairs - p0);
+    // staged input: a short first chunk (its snapshots arrive first) hides the pipeline fill
+    const int64_t first = !on_device ? std::min(c->z_pairs, std::max<int64_t>(copy_chunk * c->B, 2 * c->corr_slots / std::max(1, c->n_prn) + 1))
+                                     : c->z_pairs;
+    for (int64_t p0 = 0, np = 0; p0 < n_pairs; p0 += np) {
+        np = std::min(p0 == 0 ? first : c->z_pairs, n_pairs - p0);
         if (!on_device) {
             const int64_t last_snap = (p0 + np - 1) / c->B;
             const int64_t need = last_snap / copy_chunk;
