@@ -191,6 +191,44 @@ void gacq_trk_destroy(gacq_trk* trk);
 int gacq_trk_epl(gacq_trk* trk, const void* blocks, int64_t total_samples, int32_t n_samples,
                  const gacq_epl_chan* chans, int64_t n_chan, uint32_t flags, float* out);
 
+/* Host-side loop closure of a struct-of-arrays channel batch (tracking.py:168-275 for every
+ * channel, float64, the reference's operation order, bit-identical; no GPU needed). `sums`
+ * holds the gacq_trk_epl outputs [n][6]; the batch arrays are updated in place to the next
+ * epoch's state; out[c*3 + 0..2] = (dll_error_chips, pll_error_cycles, lock_metric).
+ * A channel whose six correlators are all zero fails with GACQ_ERR_INVALID and its index in
+ * *bad_channel (DegenerateInputError, tracking.py:173-175, 181-182). */
+typedef struct gacq_trk_batch {
+    int64_t n;
+    const int32_t* prn;
+    double* code_phase_chips;
+    double* carrier_phase_cycles;
+    double* doppler_hz;
+    double* code_rate_hz;
+    double* dll_acc;
+    double* dll_prev;
+    double* pll_acc;
+    double* pll_prev;
+    double* lock_nbd;
+    double* lock_nbp;
+    int64_t* epoch;
+    const double* sample_rate_hz;
+} gacq_trk_batch;
+
+typedef struct gacq_trk_config {
+    double integration_ms;
+    double pll_bandwidth_hz;
+    double dll_bandwidth_hz;
+    double correlator_spacing_chips;
+} gacq_trk_config;
+
+int gacq_trk_close(const float* sums, const gacq_trk_batch* batch, const gacq_trk_config* cfg, double* out,
+                   int64_t* bad_channel);
+
+/* The gacq_epl_chan records of a batch (kernels.py:56-70 NCO words; offsets[c] = first sample
+ * of channel c), for the next gacq_trk_epl. */
+int gacq_trk_chans(const gacq_trk_batch* batch, const gacq_trk_config* cfg, const int64_t* offsets,
+                   gacq_epl_chan* chans);
+
 /* Page-locked host buffers for overlapped H2D (cudaHostAlloc / cudaFreeHost). */
 int gacq_host_alloc(int64_t bytes, void** out);
 int gacq_host_free(void* ptr);

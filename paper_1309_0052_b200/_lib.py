@@ -39,6 +39,21 @@ class Sat(C.Structure):
                 ("amplitude", C.c_float), ("reserved2", C.c_float)]
 
 
+_PD = C.POINTER(C.c_double)
+
+
+class TrkBatch(C.Structure):
+    _fields_ = [("n", C.c_int64), ("prn", C.POINTER(C.c_int32)), ("code_phase_chips", _PD),
+                ("carrier_phase_cycles", _PD), ("doppler_hz", _PD), ("code_rate_hz", _PD), ("dll_acc", _PD),
+                ("dll_prev", _PD), ("pll_acc", _PD), ("pll_prev", _PD), ("lock_nbd", _PD), ("lock_nbp", _PD),
+                ("epoch", C.POINTER(C.c_int64)), ("sample_rate_hz", _PD)]
+
+
+class TrkConfig(C.Structure):
+    _fields_ = [("integration_ms", C.c_double), ("pll_bandwidth_hz", C.c_double), ("dll_bandwidth_hz", C.c_double),
+                ("correlator_spacing_chips", C.c_double)]
+
+
 class Stats(C.Structure):
     _fields_ = [("calls", C.c_int64), ("launches", C.c_int64), ("cells", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("fwd_ms", C.c_double),
@@ -52,7 +67,7 @@ ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
 EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
            "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
            "gacq_host_alloc", "gacq_host_free", "gacq_ca_code", "gacq_trk_create", "gacq_trk_destroy",
-           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth")
+           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth", "gacq_trk_close", "gacq_trk_chans")
 FMT_INT8, FMT_INT16 = 0, 1
 
 
@@ -72,6 +87,9 @@ def _load() -> C.CDLL:
                                        C.c_uint32, C.c_void_p]
     lib.gacq_power_map.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     lib.gacq_carrier_table.argtypes = [C.c_void_p, C.c_void_p]
+    lib.gacq_trk_close.argtypes = [C.c_void_p, C.POINTER(TrkBatch), C.POINTER(TrkConfig), C.c_void_p,
+                                   C.POINTER(C.c_int64)]
+    lib.gacq_trk_chans.argtypes = [C.POINTER(TrkBatch), C.POINTER(TrkConfig), C.c_void_p, C.c_void_p]
     lib.gacq_synth.argtypes = [C.c_int32, C.c_double, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_double,
                                C.c_uint64, C.c_void_p]
     lib.gacq_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]

@@ -16,7 +16,7 @@ ROOT = PKG.parent
 LIB = PKG / "libgacq.so"
 SOURCES = [PKG / "csrc" / "gacq.cu"]
 DEPS = SOURCES + [PKG / "csrc" / h for h in ("gacq_kernels.cuh", "gacq_pfa.cuh", "pfa.cuh", "pfa_tables.cuh",
-                                             "codelets.cuh", "gtrk_kernels.cuh", "gacq_tc.cuh", "tc_util.cuh", "gacq_tables.cuh", "gacq_generic.cuh", "rader31.cuh")] + [ROOT / "include" / "gacq.h"]
+                                             "codelets.cuh", "gtrk_kernels.cuh", "gacq_tc.cuh", "tc_util.cuh", "gacq_tables.cuh", "gacq_generic.cuh", "rader31.cuh", "gtrk_close.h")] + [ROOT / "include" / "gacq.h"]
 
 
 def nvcc() -> str:
@@ -28,7 +28,7 @@ def nvcc() -> str:
 
 def flags(verbose: bool = False) -> list[str]:
     f = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "--shared", "-Xcompiler", "-fPIC,-O3", "-I", str(ROOT / "include"), "-lpthread"]
+         "--shared", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-I", str(ROOT / "include"), "-lpthread"]
     if verbose:
         f += ["-Xptxas", "-v"]
     return f

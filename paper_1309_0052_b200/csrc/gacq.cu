@@ -28,6 +28,7 @@
 #include "gacq_tables.cuh"
 #include "gacq_generic.cuh"
 #include "gtrk_kernels.cuh"
+#include "gtrk_close.h"
 
 using namespace gacq;
 
@@ -1041,6 +1042,102 @@ int gacq_trk_create(gacq_trk** out, int32_t device) {
 }
 
 void gacq_trk_destroy(gacq_trk* t) { trk_free(t); }
+
+int gacq_trk_close(const float* sums, const gacq_trk_batch* b, const gacq_trk_config* cfg, double* out,
+                   int64_t* bad) {
+    using gtrk::carrier_phase_fixed; using gtrk::carrier_step_fixed; using gtrk::code_phase_fixed;
+    using gtrk::code_step_fixed; using gtrk::py_fmod; using gtrk::rint64; using gtrk::parallel_for;
+    if (!sums || !b || !cfg || !out) return fail(GACQ_ERR_INVALID, "null argument");
+    if (b->n < 1) return fail(GACQ_ERR_INVALID, "no channels");
+    const double sp = cfg->correlator_spacing_chips;
+    const double t = cfg->integration_ms * 1e-3;
+    const int64_t n = rint64(b->sample_rate_hz[0] * cfg->integration_ms * 1e-3);  // tracking.py:122-123
+    auto gains = [](double bw, double* g1, double* g2) {  // tracking.py:188-190
+        const double w0 = bw / 0.53;
+        *g1 = 2.0 * gtrk::kLoopDamping * w0;
+        *g2 = w0 * w0;
+    };
+    double g1p, g2p, g1d, g2d;
+    gains(cfg->pll_bandwidth_hz, &g1p, &g2p);
+    gains(cfg->dll_bandwidth_hz, &g1d, &g2d);
+    const double two_pi = 2.0 * 3.141592653589793;
+    const double alpha = 1.0 / gtrk::kLockSmoothing;
+    // degenerate channels first (the reference raises before touching any state): a zero
+    // prompt correlator fails the PLL discriminator (tracking.py:181-182), and with zero early
+    // and late as well the DLL one first (tracking.py:173-175)
+    for (int64_t i = 0; i < b->n; ++i) {
+        const float* s = sums + 6 * i;
+        if (s[2] == 0.f && s[3] == 0.f) {
+            if (bad) *bad = i;
+            const bool all = s[0] == 0.f && s[1] == 0.f && s[4] == 0.f && s[5] == 0.f;
+            return fail(GACQ_ERR_INVALID, "%s on channel %lld", all ? "all correlators zero" : "prompt correlator is zero",
+                        (long long)i);
+        }
+    }
+    parallel_for(b->n, [&](int64_t a, int64_t e_) {
+        for (int64_t i = a; i < e_; ++i) {
+            const float* s = sums + 6 * i;
+            const double ie = s[0], qe = s[1], ip = s[2], qp = s[3], il = s[4], ql = s[5];
+            const double e = ie * ie + qe * qe, l = il * il + ql * ql;  // tracking.py:170-171
+            const double ed = e + l == 0 ? 0.0 : (e - l) / (e + l) * (1.0 - sp / 2.0) / 2.0;
+            const double ep = ip == 0.0 ? std::copysign(0.25, qp) : std::atan(qp / ip) / two_pi;  // :179-185
+            const double fs = b->sample_rate_hz[i];
+            const double pll_acc = b->pll_acc[i] + g2p * t * (ep + b->pll_prev[i]) / 2.0;  // :198-200
+            const double dll_acc = b->dll_acc[i] + g2d * t * (ed + b->dll_prev[i]) / 2.0;
+            const double doppler = b->doppler_hz[i] + (pll_acc - b->pll_acc[i]);  // :242
+            const double code_rate = gtrk::kChipRate * (1.0 + doppler / gtrk::kL1) + dll_acc;  // :243
+            const uint64_t pc = (carrier_phase_fixed(b->carrier_phase_cycles[i]) +
+                                 (uint64_t)n * carrier_step_fixed(b->doppler_hz[i], fs) +
+                                 carrier_phase_fixed(t * g1p * ep)) % (uint64_t)gtrk::kCarrierScale;  // :211-215
+            const uint64_t nudge = (uint64_t)rint64(py_fmod(t * g1d * ed, 1023.0) * (double)gtrk::kCodeScale);
+            const uint64_t pcode = (code_phase_fixed(b->code_phase_chips[i]) +
+                                    (uint64_t)n * code_step_fixed(b->code_rate_hz[i], fs) + nudge) %
+                                   (uint64_t)gtrk::kCodeModulus;  // :218-223
+            const double nbd = ip * ip - qp * qp, nbp = ip * ip + qp * qp;  // :252-260
+            double nbd_s = nbd, nbp_s = nbp;
+            if (b->epoch[i] != 0) {
+                nbd_s = b->lock_nbd[i] + alpha * (nbd - b->lock_nbd[i]);
+                nbp_s = b->lock_nbp[i] + alpha * (nbp - b->lock_nbp[i]);
+            }
+            out[3 * i + 0] = ed;
+            out[3 * i + 1] = ep;
+            out[3 * i + 2] = nbp_s > 0 ? nbd_s / nbp_s : 0.0;
+            b->code_phase_chips[i] = (double)pcode / (double)gtrk::kCodeScale;
+            b->carrier_phase_cycles[i] = (double)pc / (double)gtrk::kCarrierScale;
+            b->doppler_hz[i] = doppler;
+            b->code_rate_hz[i] = code_rate;
+            b->dll_acc[i] = dll_acc;
+            b->dll_prev[i] = ed;
+            b->pll_acc[i] = pll_acc;
+            b->pll_prev[i] = ep;
+            b->lock_nbd[i] = nbd_s;
+            b->lock_nbp[i] = nbp_s;
+            b->epoch[i] += 1;
+        }
+    });
+    return GACQ_OK;
+}
+
+int gacq_trk_chans(const gacq_trk_batch* b, const gacq_trk_config* cfg, const int64_t* offsets, gacq_epl_chan* ch) {
+    using gtrk::carrier_phase_fixed; using gtrk::carrier_step_fixed; using gtrk::code_phase_fixed;
+    using gtrk::code_step_fixed; using gtrk::py_fmod; using gtrk::rint64; using gtrk::parallel_for;
+    if (!b || !cfg || !offsets || !ch) return fail(GACQ_ERR_INVALID, "null argument");
+    const double d = cfg->correlator_spacing_chips;
+    const double off[3] = {+d / 2, 0.0, -d / 2};  // tracking.py:148-156
+    parallel_for(b->n, [&](int64_t a, int64_t e_) {
+        for (int64_t i = a; i < e_; ++i) {
+            const double fs = b->sample_rate_hz[i];
+            ch[i].block_offset = offsets[i];
+            ch[i].carrier_p0 = carrier_phase_fixed(b->carrier_phase_cycles[i]);
+            ch[i].carrier_step = carrier_step_fixed(b->doppler_hz[i], fs);
+            for (int j = 0; j < 3; ++j) ch[i].code_p0[j] = code_phase_fixed(py_fmod(b->code_phase_chips[i] + off[j], 1023.0));
+            ch[i].code_step = code_step_fixed(b->code_rate_hz[i], fs);
+            ch[i].prn = b->prn[i];
+            ch[i].reserved = 0;
+        }
+    });
+    return GACQ_OK;
+}
 
 int gacq_trk_epl(gacq_trk* t, const void* blocks, int64_t total, int32_t n, const gacq_epl_chan* chans,
                  int64_t n_chan, uint32_t flags, float* out) {

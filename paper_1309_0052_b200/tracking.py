@@ -4,12 +4,14 @@ The receiver's step after acquisition. The O(N) per-epoch work -- carrier wipe-o
 the early / prompt / late dot products (tracking.py:126-165) -- runs on the GPU for a whole
 batch of channels in one launch (libgacq ``gacq_trk_epl``); the scalar loop math
 (discriminators, second-order loop filters, fixed-point NCO advance, lock detector,
-tracking.py:168-275) stays on the host in float64 with the reference's formulas.
+tracking.py:168-275) stays on the host in float64 with the reference's formulas: per channel
+in Python (``track_epoch``) or for a struct-of-arrays batch in libgacq's multithreaded C++
+(``gacq_trk_close`` / ``gacq_trk_chans``, used by ``track_step``).
 
-Replicas are bit-identical to the reference's (the fixed-point NCO words are computed here
-with kernels.py's exact expressions); the dot products accumulate in float64 on the device
-instead of the reference's left-to-right complex64 sum, so correlators agree to ~1e-6
-relative and the loop states to the same order.
+Replicas are bit-identical to the reference's (the fixed-point NCO words use kernels.py's
+exact expressions), the dot products follow the reference's left-to-right complex64 sums,
+and the loop closure keeps its float64 operation order, so every epoch's state equals the
+reference's bit for bit (tests/golden/tracking.json).
 """
 
 from __future__ import annotations
@@ -370,62 +372,61 @@ class TrackBatch:
                 for i in range(self.prn.size)]
 
 
+def _c_batch(batch: TrackBatch):
+    """ctypes view of a TrackBatch whose arrays are contiguous float64 / int64 / int32."""
+    d = lambda a: a.ctypes.data_as(_lib._PD)  # noqa: E731
+    return _lib.TrkBatch(batch.prn.size, batch.prn.ctypes.data_as(C.POINTER(C.c_int32)), d(batch.code_phase_chips),
+                         d(batch.carrier_phase_cycles), d(batch.doppler_hz), d(batch.code_rate_hz), d(batch.dll_acc),
+                         d(batch.dll_prev), d(batch.pll_acc), d(batch.pll_prev), d(batch.lock_nbd), d(batch.lock_nbp),
+                         batch.epoch.ctypes.data_as(C.POINTER(C.c_int64)), d(batch.sample_rate_hz))
+
+
+def _c_config(config: TrackConfig):
+    return _lib.TrkConfig(float(config.integration_ms), float(config.pll_bandwidth_hz),
+                          float(config.dll_bandwidth_hz), float(config.correlator_spacing_chips))
+
+
+def _owned(batch: TrackBatch) -> TrackBatch:
+    """A contiguous copy with the dtypes the C ABI expects."""
+    f = lambda a: np.array(a, dtype=np.float64, order="C", copy=True)  # noqa: E731
+    return TrackBatch(prn=np.array(batch.prn, dtype=np.int32, copy=True), code_phase_chips=f(batch.code_phase_chips),
+                      carrier_phase_cycles=f(batch.carrier_phase_cycles), doppler_hz=f(batch.doppler_hz),
+                      code_rate_hz=f(batch.code_rate_hz), dll_acc=f(batch.dll_acc), dll_prev=f(batch.dll_prev),
+                      pll_acc=f(batch.pll_acc), pll_prev=f(batch.pll_prev),
+                      epoch=np.array(batch.epoch, dtype=np.int64, copy=True), sample_rate_hz=f(batch.sample_rate_hz),
+                      lock_nbd=f(batch.lock_nbd), lock_nbp=f(batch.lock_nbp))
+
+
 def epl_chans(batch: TrackBatch, offsets, config: TrackConfig) -> np.ndarray:
-    """gacq_epl_chan records for every channel of the batch (vectorised kernels.py:56-70)."""
-    d = config.correlator_spacing_chips
-    ch = np.zeros(batch.prn.size, dtype=EPL_CHAN_DTYPE)
-    ch["block_offset"] = np.asarray(offsets, dtype=np.int64)
-    ch["carrier_p0"] = _carrier_phase_fixed_v(batch.carrier_phase_cycles)
-    ch["carrier_step"] = _carrier_step_fixed_v(batch.doppler_hz, batch.sample_rate_hz)
-    for j, o in enumerate((+d / 2, 0.0, -d / 2)):  # tracking.py:148-156
-        ch["code_p0"][:, j] = _code_phase_fixed_v(np.mod(batch.code_phase_chips + o, float(CODE_LENGTH)))
-    ch["code_step"] = _code_step_fixed_v(batch.code_rate_hz, batch.sample_rate_hz)
-    ch["prn"] = batch.prn
+    """gacq_epl_chan records for every channel of the batch (kernels.py:56-70, gacq_trk_chans)."""
+    b = _owned(batch)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    if off.shape != (b.prn.size,):
+        raise InvalidInputError("one block offset per channel")
+    ch = np.zeros(b.prn.size, dtype=EPL_CHAN_DTYPE)
+    cb, cc = _c_batch(b), _c_config(config)
+    _lib.check(_lib.lib.gacq_trk_chans(C.byref(cb), C.byref(cc), off.ctypes.data, ch.ctypes.data))
     return ch
 
 
 def close_loops_batch(sums: np.ndarray, batch: TrackBatch, config: TrackConfig):
     """tracking.py:231-275 over a batch, in the reference's float64 operation order
-    (bit-identical per channel; atan via math.atan). Returns (new batch, outputs dict)."""
-    ie, qe, ip, qp, il, ql = (sums[:, i].astype(np.float64) for i in range(6))
-    e = ie * ie + qe * qe
-    l = il * il + ql * ql
-    dead = (e + l == 0) & (ip == 0) & (qp == 0)
-    if dead.any():
-        raise DegenerateInputError(f"all correlators zero on channel {int(np.flatnonzero(dead)[0])}")
-    sp = config.correlator_spacing_chips
-    with np.errstate(divide="ignore", invalid="ignore"):
-        ed = np.where(e + l == 0, 0.0, (e - l) / (e + l) * (1.0 - sp / 2.0) / 2.0)
-        ratio = qp / ip
-    ep = np.array([math.copysign(0.25, q) if i == 0.0 else math.atan(r) / (2.0 * math.pi)
-                   for i, q, r in zip(ip.tolist(), qp.tolist(), ratio.tolist())], dtype=np.float64)
-    t = config.integration_ms * 1e-3
-    n = round(float(batch.sample_rate_hz[0]) * config.integration_ms * 1e-3)
-    g1p, g2p = loop_gains(config.pll_bandwidth_hz)
-    g1d, g2d = loop_gains(config.dll_bandwidth_hz)
-    pll_acc = batch.pll_acc + g2p * t * (ep + batch.pll_prev) / 2.0
-    dll_acc = batch.dll_acc + g2d * t * (ed + batch.dll_prev) / 2.0
-    doppler = batch.doppler_hz + (pll_acc - batch.pll_acc)
-    code_rate = CHIP_RATE_HZ * (1.0 + doppler / L1_CARRIER_HZ) + dll_acc
-    fs = batch.sample_rate_hz
-    pc = (_carrier_phase_fixed_v(batch.carrier_phase_cycles) + np.uint64(n) * _carrier_step_fixed_v(batch.doppler_hz, fs)
-          + _carrier_phase_fixed_v(t * g1p * ep)) % np.uint64(CARRIER_SCALE)
-    nudge = np.rint(np.mod(t * g1d * ed, float(CODE_LENGTH)) * float(CODE_SCALE)).astype(np.int64).astype(np.uint64)
-    pcode = (_code_phase_fixed_v(batch.code_phase_chips) + np.uint64(n) * _code_step_fixed_v(batch.code_rate_hz, fs)
-             + nudge) % np.uint64(CODE_MODULUS)
-    nbd = ip * ip - qp * qp
-    nbp = ip * ip + qp * qp
-    first = batch.epoch == 0
-    alpha = 1.0 / LOCK_SMOOTHING_EPOCHS
-    nbd_s = np.where(first, nbd, batch.lock_nbd + alpha * (nbd - batch.lock_nbd))
-    nbp_s = np.where(first, nbp, batch.lock_nbp + alpha * (nbp - batch.lock_nbp))
-    with np.errstate(divide="ignore", invalid="ignore"):
-        lock = np.where(nbp_s > 0, nbd_s / nbp_s, 0.0)
-    new = TrackBatch(prn=batch.prn, code_phase_chips=pcode.astype(np.float64) / float(CODE_SCALE),
-                     carrier_phase_cycles=pc.astype(np.float64) / float(CARRIER_SCALE), doppler_hz=doppler,
-                     code_rate_hz=code_rate, dll_acc=dll_acc, dll_prev=ed, pll_acc=pll_acc, pll_prev=ep,
-                     epoch=batch.epoch + 1, sample_rate_hz=fs, lock_nbd=nbd_s, lock_nbp=nbp_s)
-    outs = dict(ie=ie, qe=qe, ip=ip, qp=qp, il=il, ql=ql, dll_error_chips=ed, pll_error_cycles=ep, lock_metric=lock)
+    (bit-identical per channel; libgacq gacq_trk_close, multithreaded C++ with the C library's
+    atan, which is what math.atan calls). Returns (new batch, outputs dict)."""
+    sums = np.ascontiguousarray(sums, dtype=np.float32)
+    new = _owned(batch)
+    if sums.shape != (new.prn.size, 6):
+        raise InvalidInputError("sums must be [n_channels, 6]")
+    out = np.empty((new.prn.size, 3), dtype=np.float64)
+    bad = C.c_int64(-1)
+    cb, cc = _c_batch(new), _c_config(config)
+    rc = _lib.lib.gacq_trk_close(sums.ctypes.data, C.byref(cb), C.byref(cc), out.ctypes.data, C.byref(bad))
+    if rc == _lib.ERR_INVALID and bad.value >= 0:
+        raise DegenerateInputError((_lib.lib.gacq_last_error() or b"").decode())
+    _lib.check(rc)
+    s64 = sums.astype(np.float64)
+    outs = dict(ie=s64[:, 0], qe=s64[:, 1], ip=s64[:, 2], qp=s64[:, 3], il=s64[:, 4], ql=s64[:, 5],
+                dll_error_chips=out[:, 0], pll_error_cycles=out[:, 1], lock_metric=out[:, 2])
     return new, outs
 
 
