@@ -245,8 +245,8 @@ def measure_tracking(torch, dev, c, epochs, cpu, dist):
     ws = dist.get_world_size() if dist else 1
     res = {"metric": "tracking channel-epochs/s", "value": ws * prns.size * epochs / wall,
            "unit": "channel-epochs/s", "channels_per_gpu": int(prns.size), "epochs": epochs,
-           "note": "one gacq_trk_epl launch (all channels) + vectorised float64 loop closure per epoch; "
-                   "device-resident samples; wall-clocked"}
+           "note": "one gacq_trk_epl launch (all channels) + gacq_trk_chans/gacq_trk_close (multithreaded "
+                   "C++ float64 loop closure, bit-exact) per epoch; device-resident samples; wall-clocked"}
     if cpu:
         import oracle
 
