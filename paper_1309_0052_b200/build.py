@@ -28,7 +28,7 @@ def nvcc() -> str:
 
 def flags(verbose: bool = False) -> list[str]:
     f = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "--shared", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-I", str(ROOT / "include"), "-lpthread"]
+         "--shared", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off,-fopenmp", "-I", str(ROOT / "include"), "-lpthread", "-lgomp"]
     if verbose:
         f += ["-Xptxas", "-v"]
     return f

@@ -11,8 +11,7 @@
 #pragma once
 #include <cmath>
 #include <cstdint>
-#include <thread>
-#include <vector>
+#include <algorithm>
 
 #include "../../include/gacq.h"
 
@@ -50,21 +49,13 @@ inline uint64_t code_step_fixed(double rate, double fs) {  // kernels.py:69-70
     return (uint64_t)rint64((rate / fs) * (double)kCodeScale);
 }
 
+// channel-parallel loop on the OpenMP pool (persistent threads: no per-call spawn cost)
 template <typename F>
 inline void parallel_for(int64_t n, F&& f) {
-    const int64_t grain = 2048;
-    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(std::thread::hardware_concurrency(), (n + grain - 1) / grain));
-    if (nt == 1) {
-        f(int64_t(0), n);
-        return;
-    }
-    std::vector<std::thread> th;
-    const int64_t chunk = (n + nt - 1) / nt;
-    for (int t = 0; t < nt; ++t) {
-        const int64_t a = t * chunk, b = std::min(n, a + chunk);
-        if (a < b) th.emplace_back([&f, a, b]() { f(a, b); });
-    }
-    for (auto& x : th) x.join();
+    const int64_t grain = 1024;
+    const int64_t chunks = (n + grain - 1) / grain;
+#pragma omp parallel for schedule(static) if (chunks > 1)
+    for (int64_t c = 0; c < chunks; ++c) f(c * grain, std::min(n, (c + 1) * grain));
 }
 
 }  // namespace gtrk

@@ -217,7 +217,17 @@ class TrackEngine:
         _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, n, chans, len(states), flags, out.ctypes.data))
         return out
 
-    def correlate_chans(self, samples, chans: np.ndarray, n: int) -> np.ndarray:
+    def pinned(self, n_chan: int):
+        """Page-locked (chans [n], sums [n, 6]) views reused across epochs (fast H2D/D2H)."""
+        from .acquisition import PinnedBuffer
+
+        if getattr(self, "_pin_n", 0) < n_chan:
+            self._pin_chans = PinnedBuffer((n_chan,), EPL_CHAN_DTYPE)
+            self._pin_sums = PinnedBuffer((n_chan, 6), np.float32)
+            self._pin_n = n_chan
+        return self._pin_chans.array[:n_chan], self._pin_sums.array[:n_chan]
+
+    def correlate_chans(self, samples, chans: np.ndarray, n: int, out: np.ndarray | None = None) -> np.ndarray:
         """Like correlate() but from prepared gacq_epl_chan records (tracking.EPL_CHAN_DTYPE)."""
         chans = np.ascontiguousarray(chans)
         cai = getattr(samples, "__cuda_array_interface__", None)
@@ -228,7 +238,8 @@ class TrackEngine:
         else:
             arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
             total, ptr, flags = arr.size, arr.ctypes.data, 0
-        out = np.empty((chans.size, 6), dtype=np.float32)
+        if out is None:
+            out = np.empty((chans.size, 6), dtype=np.float32)
         _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, int(n), chans.ctypes.data, chans.size, flags,
                                          out.ctypes.data))
         return out
@@ -433,10 +444,16 @@ def close_loops_batch(sums: np.ndarray, batch: TrackBatch, config: TrackConfig):
 def track_step(samples, offsets, batch: TrackBatch, config: TrackConfig, device: int = 0):
     """One epoch of a struct-of-arrays batch: one device launch + vectorised loop closure."""
     eng = get_track_engine(device)
-    chans = epl_chans(batch, offsets, config)
-    n = round(float(batch.sample_rate_hz[0]) * config.integration_ms * 1e-3)
-    sums = eng.correlate_chans(samples, chans, n)
-    return close_loops_batch(sums, batch, config)
+    b = _owned(batch)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    if off.shape != (b.prn.size,):
+        raise InvalidInputError("one block offset per channel")
+    chans, sums = eng.pinned(b.prn.size)  # page-locked: the per-epoch H2D / D2H run at full speed
+    cb, cc = _c_batch(b), _c_config(config)
+    _lib.check(_lib.lib.gacq_trk_chans(C.byref(cb), C.byref(cc), off.ctypes.data, chans.ctypes.data))
+    n = round(float(b.sample_rate_hz[0]) * config.integration_ms * 1e-3)
+    eng.correlate_chans(samples, chans, n, out=sums)
+    return close_loops_batch(sums, b, config)
 
 
 def track_epoch_batch(samples, offsets, states, config: TrackConfig, device: int = 0):
