@@ -264,3 +264,22 @@ def test_generic_rates_use_the_generic_path(pkg):
     eng = pkg.AcqEngine(4.092e6, [1], pkg.AcqConfig(noncoherent_rounds=1))
     assert eng.info["path"] == 2
     eng.close()
+
+
+@pytest.mark.parametrize("n_snap", [1, 3, 17, 40])
+def test_chunked_staging_matches_device_resident(pkg, n_snap):
+    # a small spectrum scratch forces many compute chunks (a short first one, then full ones)
+    # and 16-snapshot copy events; staged host input and device input give identical rows
+    import torch
+
+    cs = [case(f"c3_snap{i}") for i in range(8)]
+    host = np.stack([case_input(cs[i % 8]) for i in range(n_snap)])
+    small = pkg.AcqEngine(cs[0]["fs"], cs[0]["prns"], to_cfg(pkg, cs[0]), scratch_bytes=24 << 20)
+    big = pkg.get_engine(cs[0]["fs"], cs[0]["prns"], to_cfg(pkg, cs[0]))
+    ref = big.run_rows(torch.from_numpy(host).cuda())
+    np.testing.assert_array_equal(small.run_rows(host), ref)
+    pinned = pkg.PinnedBuffer(host.shape)
+    pinned.array[...] = host
+    np.testing.assert_array_equal(small.run_rows(pinned.array), ref)
+    pinned.close()
+    small.close()
