@@ -168,6 +168,30 @@ __device__ __forceinline__ void wipe_fold(const cx* __restrict__ x, const cx* __
 #define GACQ_WIPE_U 4
 #endif
         constexpr int U = GACQ_WIPE_U;  // 16-byte load pairs in flight per thread
+        if (K == 1) {  // one code period per block (coherent_ms = 1): no fold, twice the loads in flight
+            constexpr int U1 = 2 * U;
+            for (int base = threadIdx.x; base < np; base += U1 * NT) {
+                ulonglong2 xv[U1], cv[U1];
+#pragma unroll
+                for (int u = 0; u < U1; ++u) {
+                    const int i = base + u * NT;
+                    if (i < np) {
+                        xv[u] = __ldg(x2 + i);
+                        cv[u] = __ldg(c2 + i);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U1; ++u) {
+                    const int i = base + u * NT;
+                    if (i < np) {
+                        put(2 * i, cmul_exact(xv[u].x, cv[u].x));
+                        put(2 * i + 1, cmul_exact(xv[u].y, cv[u].y));
+                    }
+                }
+            }
+            __syncthreads();
+            return;
+        }
         for (int base = threadIdx.x; base < np; base += U * NT) {
             cx w[U][2];
             for (int k = 0; k < K; ++k) {

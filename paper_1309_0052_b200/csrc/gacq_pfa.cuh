@@ -77,7 +77,9 @@ __device__ __forceinline__ float pow_acc(cx v, float acc) { return fmaf(im(v), i
 
 // ---- K1 ---------------------------------------------------------------------------------
 #ifndef GACQ_FWD_MINB
-#define GACQ_FWD_MINB(W) (16 / (W) > 0 ? 16 / (W) : 1)  // <= 128 registers: 16 warps per SM
+// <= 128 registers (16 warps per SM) where shared memory allows several CTAs; the D >= 13
+// variants (131 KB wiped-block table) run one CTA per SM and get the full register file
+#define GACQ_FWD_MINB(D, W) ((D) >= 13 ? 1 : 16 / (W) > 0 ? 16 / (W) : 1)
 #endif
 struct FwdPfaArgs {
     const float2* snaps;   // batch base (device), snapshot s at snaps + s*stride
@@ -92,7 +94,7 @@ struct FwdPfaArgs {
 // phases rho in [w PWF, (w+1) PWF), PWF = ceil(D/W), sliding the chip sums by one sample per
 // phase. dynamic smem: fwd_pfa_smem(D, W).
 template <int D, int W>
-__global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(W)) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
+__global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kernel(FwdPfaArgs a) {
     constexpr int WS = fwd_ws(D);
     constexpr int PWF = (D + W - 1) / W;
     extern __shared__ __align__(16) cx smem[];
