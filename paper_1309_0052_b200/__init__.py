@@ -12,10 +12,12 @@ from .acquisition import (  # noqa: F401
     PinnedBuffer,
     acquire_all,
     acquire_batch,
+    acquire_bins_sharded,
     acquire_channel,
     acquire_if_file,
     default_doppler_step_hz,
     get_engine,
+    merge_bin_shards,
     samples_per_code_period,
 )
 from .buffers import IqBuffer, Precision  # noqa: F401

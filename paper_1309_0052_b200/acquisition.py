@@ -115,6 +115,21 @@ class BatchResult:
         return out
 
 
+def _finish(rows: np.ndarray, prns: np.ndarray, bins: np.ndarray, config: AcqConfig, mults: int) -> BatchResult:
+    """acquisition.py:160-170 over grid-global rows: metric = float64(peak)/float64(floor)
+    (inf when floor == 0), detected = metric >= threshold, doppler = bins[bin]."""
+    peak = rows["peak"]
+    floor = rows["floor"]
+    p64, f64 = peak.astype(np.float64), floor.astype(np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        metric = np.where(f64 > 0, p64 / np.where(f64 > 0, f64, 1.0), np.inf)
+    b = rows["bin"]
+    return BatchResult(prns=prns.copy(), bin_index=b, doppler_hz=bins[b],
+                       code_phase_samples=rows["lag"].astype(np.int64), peak=peak, floor=floor,
+                       peak_metric=metric, detected=metric >= config.detection_threshold,
+                       bins_searched=int(bins.size), multiplications_performed=mults)
+
+
 def _host_array(x) -> np.ndarray:
     arr = np.asarray(x)
     if arr.dtype != np.complex64:
@@ -160,7 +175,10 @@ class AcqEngine:
     """A search plan bound to one CUDA device (reference: acquire_all's per-call state)."""
 
     def __init__(self, sample_rate_hz: float, prns, config: AcqConfig | None = None,
-                 device: int = 0, scratch_bytes: int = 0):
+                 device: int = 0, scratch_bytes: int = 0, bin_range: tuple | None = None):
+        """``bin_range=(b0, b1)`` searches only bins [b0, b1) of the config's grid (Doppler-bin
+        sharding of one snapshot over devices); rows then carry grid-global
+        bin indices, so per-shard rows merge with ``merge_bin_shards``."""
         config = config or AcqConfig()
         prns = [int(p) for p in prns]
         if not prns:
@@ -178,14 +196,18 @@ class AcqEngine:
         self.prns = np.asarray(prns, dtype=np.int32)
         self.device = int(device)
         self.bins = config.doppler_bins_hz()
+        b0, b1 = (0, self.bins.size) if bin_range is None else (int(bin_range[0]), int(bin_range[1]))
+        if not 0 <= b0 < b1 <= self.bins.size:
+            raise InvalidInputError(f"bin_range {bin_range} outside the {self.bins.size}-bin grid")
+        self.bin0 = b0
         self.n_coh = round(fs * config.coherent_ms * 1e-3)
         self.period = samples_per_code_period(fs)
         if self.n_coh < self.period:
             raise InvalidInputError("coherent window shorter than one code period")
         self.span = self.n_coh * config.noncoherent_rounds
         self.radius = config.exclusion_radius_samples or math.ceil(fs / CHIP_RATE_HZ)
-        self._bins_c = np.ascontiguousarray(self.bins, dtype=np.float64)
-        params = _lib.Params(fs, config.coherent_ms, config.noncoherent_rounds, self.bins.size,
+        self._bins_c = np.ascontiguousarray(self.bins[b0:b1], dtype=np.float64)
+        params = _lib.Params(fs, config.coherent_ms, config.noncoherent_rounds, self._bins_c.size,
                              self._bins_c.ctypes.data_as(C.POINTER(C.c_double)), self.radius,
                              len(prns), self.prns.ctypes.data_as(C.POINTER(C.c_int32)), self.device,
                              0, int(scratch_bytes))
@@ -223,26 +245,19 @@ class AcqEngine:
         if n_samp < self.span:
             raise InvalidInputError(f"buffer holds {n_samp} samples, {self.span} needed for the "
                                     "configured integration")
-        shape = (n_snap, self.prns.size) + ((self.bins.size,) if per_bin else ())
+        shape = (n_snap, self.prns.size) + ((self._bins_c.size,) if per_bin else ())
         if out is None:
             out = np.empty(shape, dtype=_lib.ROW_DTYPE)
         elif out.shape != shape or out.dtype != np.dtype(_lib.ROW_DTYPE) or not out.flags.c_contiguous:
             raise InvalidInputError("bad output row buffer")
         _lib.check(_lib.lib.gacq_run(self._ctx, ptr, n_snap, stride, flags, out.ctypes.data))
+        if self.bin0:
+            out["bin"] += self.bin0
         return out
 
     def finish(self, rows: np.ndarray) -> BatchResult:
         """acquisition.py:160-170 over a row array, vectorised (float64 ratio, >= threshold)."""
-        peak = rows["peak"]
-        floor = rows["floor"]
-        p64, f64 = peak.astype(np.float64), floor.astype(np.float64)
-        with np.errstate(divide="ignore", invalid="ignore"):
-            metric = np.where(f64 > 0, p64 / np.where(f64 > 0, f64, 1.0), np.inf)
-        b = rows["bin"]
-        return BatchResult(prns=self.prns.copy(), bin_index=b, doppler_hz=self.bins[b],
-                           code_phase_samples=rows["lag"].astype(np.int64), peak=peak, floor=floor,
-                           peak_metric=metric, detected=metric >= self.config.detection_threshold,
-                           bins_searched=int(self.bins.size), multiplications_performed=self.mults)
+        return _finish(rows, self.prns, self.bins, self.config, self.mults)
 
     def search(self, snapshots, profile: bool = False) -> BatchResult:
         return self.finish(self.run_rows(snapshots, profile=profile))
@@ -280,9 +295,11 @@ class AcqEngine:
         if n_vals // 2 < self.span:
             raise InvalidInputError(f"buffer holds {n_vals // 2} samples, {self.span} needed for the "
                                     "configured integration")
-        out = np.empty((n_snap, self.prns.size) + ((self.bins.size,) if per_bin else ()), dtype=_lib.ROW_DTYPE)
+        out = np.empty((n_snap, self.prns.size) + ((self._bins_c.size,) if per_bin else ()), dtype=_lib.ROW_DTYPE)
         _lib.check(_lib.lib.gacq_run_quantized(self._ctx, ptr, int(sample_format), float(scale), n_snap, row // 2,
                                                flags, out.ctypes.data))
+        if self.bin0:
+            out["bin"] += self.bin0
         return out
 
     def search_quantized(self, iq, sample_format: int, scale: float, profile: bool = False) -> BatchResult:
@@ -290,7 +307,7 @@ class AcqEngine:
 
     def carrier_table(self) -> np.ndarray:
         """complex64 [n_bins, n_coh] wipe-off replicas the device built (parity hook)."""
-        out = np.empty((self.bins.size, self.info["n_coh"]), dtype=np.complex64)
+        out = np.empty((self._bins_c.size, self.info["n_coh"]), dtype=np.complex64)
         _lib.check(_lib.lib.gacq_carrier_table(self._ctx, out.ctypes.data))
         return out
 
@@ -300,7 +317,7 @@ class AcqEngine:
         if arr.shape[1] < self.span:
             raise InvalidInputError("snapshot too short for the configured integration")
         x = np.ascontiguousarray(arr[0, :self.span])
-        out = np.empty((self.prns.size, self.bins.size, self.period), dtype=np.float32)
+        out = np.empty((self.prns.size, self._bins_c.size, self.period), dtype=np.float32)
         _lib.check(_lib.lib.gacq_power_map(self._ctx, x.ctypes.data, out.ctypes.data))
         return out
 
@@ -430,6 +447,55 @@ def acquire_batch(snapshots, sample_rate_hz: float, prns, config: AcqConfig | No
     if errs:
         raise errs[0]
     return [r for o in outs for r in o]
+
+
+def merge_bin_shards(shard_rows) -> np.ndarray:
+    """Merge per-shard rows [n_snap, n_prn] (grid-global bin indices, shards in ascending bin
+    order) into the rows of the whole grid: the larger peak wins, ties go to the earlier
+    shard, i.e. the lower bin -- the reference's row-major first argmax (acquisition.py:151).
+    The winning row's floor travels with it, since the floor is row-local."""
+    shard_rows = [np.asarray(r) for r in shard_rows]
+    out = shard_rows[0].copy()
+    for r in shard_rows[1:]:
+        take = r["peak"] > out["peak"]
+        out[take] = r[take]
+    return out
+
+
+def acquire_bins_sharded(snapshots, sample_rate_hz: float, prns, config: AcqConfig | None = None,
+                         devices=None) -> BatchResult:
+    """One (or a few) large snapshots searched with the Doppler grid split into contiguous
+    bin ranges, one per device (the C2/C4 single-snapshot case), one host
+    thread per device; the per-shard rows are merged exactly (merge_bin_shards)."""
+    config = config or AcqConfig()
+    arr = _host_array(snapshots)
+    devices = list(devices) if devices else [0]
+    n_bins = config.doppler_bins_hz().size
+    ranges = [r for r in np.array_split(np.arange(n_bins), len(devices)) if r.size]
+    engines = [AcqEngine(sample_rate_hz, prns, config, d, bin_range=(int(r[0]), int(r[-1]) + 1))
+               for d, r in zip(devices, ranges)]
+    outs: list = [None] * len(engines)
+    errs: list = []
+
+    def work(i):
+        try:
+            outs[i] = engines[i].run_rows(arr)
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            errs.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(engines))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    try:
+        if errs:
+            raise errs[0]
+        e0 = engines[0]
+        return _finish(merge_bin_shards(outs), e0.prns, e0.bins, config, e0.mults)
+    finally:
+        for e in engines:
+            e.close()
 
 
 def acquire_if_file(path, prns, config: AcqConfig | None = None, device: int = 0) -> list:

@@ -93,3 +93,26 @@ def test_single_process_passthrough():
     rows = FakeEngine().run_rows(np.zeros((4, 8), dtype=np.complex64))
     assert gather_rows(rows, 4, None) is rows
     assert max_over_ranks(3.5) == 3.5
+
+
+def test_merge_bin_shards_is_the_row_major_first_argmax():
+    # merging per-shard rows (grid-global bins, ascending shards) equals the argmax over the
+    # concatenated grid: larger peak wins, ties go to the lower bin, the floor travels with it
+    from paper_1309_0052_b200 import _lib, merge_bin_shards
+
+    rng = np.random.default_rng(3)
+    n_snap, n_prn, n_bins = 5, 7, 21
+    per_bin = np.zeros((n_snap, n_prn, n_bins), dtype=_lib.ROW_DTYPE)
+    per_bin["bin"] = np.arange(n_bins)
+    per_bin["lag"] = rng.integers(0, 4092, per_bin.shape)
+    per_bin["peak"] = rng.integers(0, 6, per_bin.shape).astype(np.float32)  # many exact ties
+    per_bin["floor"] = rng.random(per_bin.shape).astype(np.float32)
+    want = per_bin[np.arange(n_snap)[:, None], np.arange(n_prn)[None, :], np.argmax(per_bin["peak"], axis=2)]
+    for cuts in ([0, 7, 14, 21], [0, 1, 21], [0, 10, 11, 20, 21]):
+        shards = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            sub = per_bin[:, :, a:b]
+            k = np.argmax(sub["peak"], axis=2)
+            shards.append(sub[np.arange(n_snap)[:, None], np.arange(n_prn)[None, :], k])
+        got = merge_bin_shards(shards)
+        np.testing.assert_array_equal(got, want)
