@@ -47,6 +47,9 @@ CONFIGS = {
                desc="C2: 10 ms snapshots @4.092 MHz, 32 PRNs x 41 bins (+-5 kHz/250 Hz), 10 x 1 ms noncoherent"),
     "c3": dict(fs=4.092e6, rounds=10, step=500.0, span_hz=5000.0, batch=1024,
                desc="C3: 10 ms snapshots @4.092 MHz, 32 PRNs x 21 bins (+-5 kHz/500 Hz), 10 x 1 ms noncoherent"),
+    "d8": dict(fs=8.184e6, rounds=10, step=2.0 / 3.0 / 1e-3, span_hz=5000.0, batch=512,
+               desc="D8: the reference's default acquisition (8.184 MHz, AcqConfig(): 16 bins of 666.7 Hz, "
+                    "10 x 1 ms noncoherent), 32 PRNs"),
     "g5": dict(fs=5.0e6, rounds=10, step=500.0, span_hz=5000.0, batch=64,
                desc="G5: 10 ms snapshots @5 MHz (not chip-aligned: generic power-of-two path), 32 PRNs x 21 bins, "
                     "10 x 1 ms noncoherent"),
