@@ -299,3 +299,31 @@ def test_doppler_bin_sharding_equals_whole_grid(pkg, name, n_dev):
     for g, r in zip(shard.results()[0], c["results"]):
         assert (g.doppler_hz, g.code_phase_samples, g.detected) == (r["doppler_hz"], r["code_phase_samples"],
                                                                     r["detected"])
+
+
+def test_concurrent_host_threads_on_one_plan(pkg):
+    # calls on one context are serialized inside libgacq (the GIL is released by ctypes), so
+    # several host threads sharing a plan get exactly the sequential answers
+    import threading
+
+    cs = [case(f"c3_snap{i}") for i in range(8)]
+    eng = pkg.get_engine(cs[0]["fs"], cs[0]["prns"], to_cfg(pkg, cs[0]))
+    xs = [case_input(c) for c in cs]
+    want = [eng.run_rows(x) for x in xs]
+    got = [None] * 32
+    errs = []
+
+    def work(i):
+        try:
+            got[i] = eng.run_rows(xs[i % 8])
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(32)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs[0]
+    for i in range(32):
+        np.testing.assert_array_equal(got[i], want[i % 8])
