@@ -291,6 +291,14 @@ def run_ours(args, rank, world, local_rank):
         cpu_baseline = {"value": rates[0], "unit": UNIT, "cores": workers, "kind": "port", "sample": sample}
 
     torch.cuda.set_device(local_rank)
+    if world > 1:  # share the host cores between the ranks of this node (libgacq's OpenMP loops)
+        try:
+            import ctypes
+
+            per_rank = max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+            ctypes.CDLL("libgomp.so.1").omp_set_num_threads(per_rank)
+        except OSError:
+            pass
     dist = None
     if world > 1:
         import torch.distributed as dist
