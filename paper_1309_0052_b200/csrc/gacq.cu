@@ -238,6 +238,7 @@ void corr_pfa_shape(int D, int* W, int* PW) {
 
 cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
+    if (ca.n_items + c->corr_slots >= INT32_MAX) return cudaErrorInvalidValue;  // 32-bit item indices
     if (c->tc) {
         const float4* B = reinterpret_cast<const float4*>(c->d_tcB);
         if (c->cpw == 1)

@@ -220,10 +220,13 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         mbar_init(&mbar[1], 1);
         fence_mbar_init();
     }
-    int64_t item = blockIdx.x;
-    if (item >= a.n_items) return;
-    auto load_cc = [&](int64_t it) {  // cp.async of the half spectrum of item `it`'s PRN
-        const char* g = reinterpret_cast<const char*>(a.Cc + (it % a.n_prn) * kCcHalf);
+    // item indices fit 32 bits (launch_corr_pfa checks): unsigned 32-bit divisions per item
+    const int n_items = (int)a.n_items;
+    const unsigned n_prn = (unsigned)a.n_prn;
+    int item = blockIdx.x;
+    if (item >= n_items) return;
+    auto load_cc = [&](int it) {  // cp.async of the half spectrum of item `it`'s PRN
+        const char* g = reinterpret_cast<const char*>(a.Cc + ((unsigned)it % n_prn) * kCcHalf);
         for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(ccs + 2 * i, g + 16 * i);
         cp_async_commit();
     };
@@ -233,7 +236,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     const int rho0 = w * a.PW;
     const int nph = min(a.PW, a.D - rho0);  // phases of this warp
     const int64_t pair_span = (int64_t)a.R * a.D * kBuf;
-    auto zbase = [&](int64_t it) { return a.Z + (it / a.n_prn) * pair_span + rho0 * kBuf; };
+    auto zbase = [&](int it) { return a.Z + (int64_t)((unsigned)it / n_prn) * pair_span + rho0 * kBuf; };
     unsigned t = 0;  // this warp's transform count: buffer t & 1, mbarrier parity (t >> 1) & 1
     __syncwarp();
     if (lane == 0) bulk_load(buf, zbase(item), kSpecBytes, &mbar[0]);
@@ -241,15 +244,15 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     const int pl = lane == 0 ? 0 : 31 - lane;  // Hermitian partner column of k1 = lane
     cp_async_wait_all();
     __syncthreads();
-    int64_t next = s_claim0;  // s_claim itself is rewritten by thread 0 at the end of the first item
+    int next = (int)s_claim0;  // s_claim itself is rewritten by thread 0 at the end of the first item
 
     for (;;) {
         long long claim = 0;
-        if (threadIdx.x == 0 && next < a.n_items) claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
-        const int64_t lp = item / a.n_prn;
-        const int pi = (int)(item % a.n_prn);
-        const cx* zb = zbase(item);
-        const cx* zn = next < a.n_items ? zbase(next) : nullptr;
+        if (threadIdx.x == 0 && next < n_items) claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
+        const unsigned lp = (unsigned)item / n_prn;
+        const int pi = (int)((unsigned)item - lp * n_prn);
+        const cx* zb = a.Z + (int64_t)lp * pair_span + rho0 * kBuf;
+        const cx* zn = next < n_items ? zbase(next) : nullptr;
 
         float best = -1.f;
         int bidx = 0x7fffffff;
@@ -349,7 +352,18 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
             int bl = 0x7fffffff;
-            if (lane_max == m) for_cells([&](float v, int lag) { if (v == m && lag < bl) bl = lag; });
+            if (lane_max == m) {  // cells equal to the max as a mask; lags only for its set bits
+                unsigned mk = 0u;
+#pragma unroll
+                for (int q1 = 0; q1 < 31; ++q1) mk |= (acc[q1] == m ? 1u : 0u) << q1;
+                while (mk) {
+                    const int q1 = __ffs(mk) - 1;
+                    mk &= mk - 1u;
+                    bl = min(bl, a.D * cell_q(q1, lane) + rho0);
+                }
+                if (x0 && accx[0] == m) bl = min(bl, a.D * cell_q(lane == 16 ? 0 : lane, 32) + rho0);
+                if (x1 && accx[1] == m) bl = min(bl, a.D * cell_q(31 - lane, 32) + rho0);
+            }
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) bl = min(bl, __shfl_xor_sync(0xffffffffu, bl, off));
             best = m;
@@ -365,18 +379,15 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
         if (threadIdx.x == 0) s_claim = claim;
         __syncthreads();  // every warp is done with this item's spectra, Cc and row spills
-        const int64_t after = s_claim;
-        if (next < a.n_items) load_cc(next);  // lands while the floor is computed
+        const int after = (int)s_claim;
+        if (next < n_items) load_cc(next);  // lands while the floor is computed
         best = red_v[0];
         bidx = red_i[0];
         for (int i = 1; i < W; ++i)
             if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
         const int peak = bidx;
         // exclusion floor (acquisition.py:155-159)
-        const int64_t pair = a.pair0 + lp;
-        const int64_t s = pair / a.B;
-        const int b = (int)(pair % a.B);
-        float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
+        float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + (a.pair0 + lp) % a.B) * a.P : nullptr;
         float fl = -1.f;
         if (kRegs && !pm) {
             // Only the cells within `radius` of the peak are excluded: lags D q + rho0 for q in
@@ -384,9 +395,10 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
             // of them. Cell q lives at (q1, q2) = (16 q mod 31, 16 q mod 33) (inverse of cell_q).
             // A lane with none of them takes its plain max.
             if (2 * a.radius + 1 < a.P) {
-                const int lo = peak - a.radius - rho0, hi = peak + a.radius - rho0;
-                const int qa = lo >= 0 ? (lo + a.D - 1) / a.D : -(-lo / a.D);
-                const int qb = hi >= 0 ? hi / a.D : -((-hi + a.D - 1) / a.D);
+                // offset by D * 1023 (> radius + rho0) so both bounds divide as unsigned
+                const unsigned off = (unsigned)(a.D * kChips), D = (unsigned)a.D;
+                const unsigned lo = (unsigned)(peak - a.radius - rho0) + off, hi = (unsigned)(peak + a.radius - rho0) + off;
+                const int qa = (int)((lo + D - 1u) / D) - kChips, qb = (int)(hi / D) - kChips;
                 unsigned m31 = 0u, mx = 0u;
                 for (int q = qa; q <= qb; ++q) {
                     const int qq = q < 0 ? q + kChips : q >= kChips ? q - kChips : q;
@@ -430,6 +442,9 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         if (threadIdx.x == 0) {
             float f = red_f[0];
             for (int i = 1; i < W; ++i) f = fmaxf(f, red_f[i]);
+            const int64_t pair = a.pair0 + lp;
+            const int64_t s = pair / a.B;
+            const int b = (int)(pair - s * a.B);
             gacq_row out;
             out.bin = b;
             out.lag = peak;
@@ -439,7 +454,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         }
         item = next;
         next = after;
-        if (item >= a.n_items) break;
+        if (item >= n_items) break;
     }
 }
 
