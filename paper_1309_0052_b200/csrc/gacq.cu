@@ -407,7 +407,8 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             CUDA_TRY(cudaGetLastError());
         } else if (c->pfa) {
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
-                           np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw, 0};
+                           np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw, 0,
+                           (unsigned)(((1ull << 32) + c->D - 1) / c->D)};
             CUDA_TRY(launch_corr_pfa(c, ca));
         } else {
             CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, np * c->n_prn,

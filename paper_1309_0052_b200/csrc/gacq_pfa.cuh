@@ -181,6 +181,7 @@ struct CorrPfaArgs {
     unsigned long long* counter;  // zeroed before the launch
     int B, R, D, P, n_prn, radius, PW;
     int zero;              // 0 (an opaque runtime zero, see dft31_stream)
+    unsigned dmagic;       // ceil(2^32 / D): x / D == umulhi(x, dmagic) for x < 2^32 / D
 };
 
 // chip lag of cell (q1, q2)
@@ -189,6 +190,11 @@ __device__ __forceinline__ int cell_q(int q1, int q2) {
     return q >= 2 * kChips ? q - 2 * kChips : q >= kChips ? q - kChips : q;
 }
 __device__ __forceinline__ bool better(float v, int l, float bv, int bl) { return v > bv || (v == bv && l < bl); }
+// (power >= 0, lag >= 0) as one unsigned key ordered like better(): the bits of a non-negative
+// float order like its value, and the low word inverts the lag so ties go to the lowest lag
+__device__ __forceinline__ unsigned long long peak_key(float v, int lag) {
+    return ((unsigned long long)__float_as_uint(v) << 32) | (0xffffffffu - (unsigned)lag);
+}
 __device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
     int d = abs(lag - peak);
     d = min(d, P - d);
@@ -205,8 +211,8 @@ __device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
 // dynamic smem: corr_pfa_smem(W).
 template <bool kRegs>
 __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
-    __shared__ float red_v[kCorrMaxWarps], red_f[kCorrMaxWarps];
-    __shared__ int red_i[kCorrMaxWarps];
+    __shared__ unsigned long long red_k[kCorrMaxWarps];  // per-warp (peak, lag) keys, see peak_key
+    __shared__ float red_f[kCorrMaxWarps];
     __shared__ long long s_claim, s_claim0;  // s_claim0: the first claim (read before the item loop)
     __shared__ float s_coef[15][32];  // coop31 columns, read conflict-free as s_coef[j-1][lane]
     extern __shared__ __align__(16) cx smem[];
@@ -376,16 +382,15 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
             }
         }
-        if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
+        if (lane == 0) red_k[w] = peak_key(best, bidx);
         if (threadIdx.x == 0) s_claim = claim;
         __syncthreads();  // every warp is done with this item's spectra, Cc and row spills
         const int after = (int)s_claim;
         if (next < n_items) load_cc(next);  // lands while the floor is computed
-        best = red_v[0];
-        bidx = red_i[0];
-        for (int i = 1; i < W; ++i)
-            if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
-        const int peak = bidx;
+        unsigned long long kb = red_k[0];
+        for (int i = 1; i < W; ++i) kb = max(kb, red_k[i]);
+        best = __uint_as_float((unsigned)(kb >> 32));
+        const int peak = (int)(0xffffffffu - (unsigned)kb);
         // exclusion floor (acquisition.py:155-159)
         float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + (a.pair0 + lp) % a.B) * a.P : nullptr;
         float fl = -1.f;
@@ -398,7 +403,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 // offset by D * 1023 (> radius + rho0) so both bounds divide as unsigned
                 const unsigned off = (unsigned)(a.D * kChips), D = (unsigned)a.D;
                 const unsigned lo = (unsigned)(peak - a.radius - rho0) + off, hi = (unsigned)(peak + a.radius - rho0) + off;
-                const int qa = (int)((lo + D - 1u) / D) - kChips, qb = (int)(hi / D) - kChips;
+                const int qa = (int)__umulhi(lo + D - 1u, a.dmagic) - kChips, qb = (int)__umulhi(hi, a.dmagic) - kChips;
                 unsigned m31 = 0u, mx = 0u;
                 for (int q = qa; q <= qb; ++q) {
                     const int qq = q < 0 ? q + kChips : q >= kChips ? q - kChips : q;
