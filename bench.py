@@ -53,6 +53,9 @@ CONFIGS = {
     "g5": dict(fs=5.0e6, rounds=10, step=500.0, span_hz=5000.0, batch=64,
                desc="G5: 10 ms snapshots @5 MHz (not chip-aligned: generic power-of-two path), 32 PRNs x 21 bins, "
                     "10 x 1 ms noncoherent"),
+    "g8": dict(fs=8.192e6, rounds=10, step=500.0, span_hz=5000.0, batch=64,
+               desc="G8: 10 ms snapshots @8.192 MHz (not chip-aligned; n_coh = 8192 runs as the circular "
+                    "8192-point transform), 32 PRNs x 21 bins, 10 x 1 ms noncoherent"),
     "c4": dict(fs=16.368e6, rounds=20, step=125.0, span_hz=10000.0, batch=16,
                desc="C4: 20 ms snapshots @16.368 MHz, 32 PRNs x 161 bins (+-10 kHz/125 Hz), 20 x 1 ms noncoherent"),
 }

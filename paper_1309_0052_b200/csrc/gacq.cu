@@ -543,7 +543,13 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     const bool gen = !aligned || (path_env && std::strcmp(path_env, "generic") == 0);
     int logM = 0;
     if (gen) {
-        while ((int64_t(1) << logM) < n_coh + P - 1) ++logM;
+        // n_coh a power of two: the reference's n_coh-point circular correlation is the M = n_coh
+        // transform itself (no extension), when the correlation kernel's lag capacity
+        // (L kGenMaxM / 2) holds P; otherwise the linear form with M >= n_coh + P - 1
+        while ((int64_t(1) << logM) < n_coh) ++logM;
+        const int64_t lag_cap = (int64_t)(logM > kGenMaxLogM ? 2 : 1) * kGenMaxM / 2;
+        if ((int64_t(1) << logM) != n_coh || P > lag_cap)
+            while ((int64_t(1) << logM) < n_coh + P - 1) ++logM;
         if (logM > kGenMaxLogMTotal)
             return fail(GACQ_ERR_UNSUPPORTED,
                         "fs=%.17g Hz, coherent_ms=%d: the generic path's transform (%lld points >= n_coh + P - 1) "

@@ -10,6 +10,9 @@
 //   w_ext[j] = w[j mod N] (j < N + P - 1), zero beyond,   c = the sampled code replica
 //   r = IDFT_M( DFT_M(w_ext) . conj(DFT_M(c)) / M )[0, P)      (no index wrap for tau < P)
 // so no rescale is needed (the reference's ifft carries 1/N, the table carries 1/M).
+// When N is itself a power of two (e.g. 8.192 MHz) the plan takes M = N: the transform is then
+// the reference's circular correlation directly (j < M = N never reaches the extension), as
+// long as P fits the correlation kernel's lag capacity L kGenMaxM / 2.
 //
 //   K1 gacq_gen_fwd_kernel : per (snapshot, bin, round): bit-exact wipe-off (kernels.py:78-86),
 //                            periodic extension, zero padding, forward M-point FFT -> Z.

@@ -96,9 +96,10 @@ def test_create_rejects_oversized_generic_rate_before_touching_a_device(pkg):
     # exceeds the two-CTA limit: refused loudly, never a CPU path
     with pytest.raises(pkg.UnsupportedError, match="generic path"):
         pkg.AcqEngine(20e6, [1], pkg.AcqConfig())
-    # 8.192 MHz with 4 ms coherent: 32768 + 8192 - 1 points -> 65536, also refused
+    # 8.192 MHz with 5 ms coherent: 40960 + 8192 - 1 points -> 65536, also refused (4 ms,
+    # n_coh = 32768, is a power of two and runs as the 32768-point circular transform)
     with pytest.raises(pkg.UnsupportedError, match="generic path"):
-        pkg.AcqEngine(8.192e6, [1], pkg.AcqConfig(coherent_ms=4))
+        pkg.AcqEngine(8.192e6, [1], pkg.AcqConfig(coherent_ms=5))
 
 
 def test_create_without_gpu_raises_resource_error(pkg):

@@ -266,6 +266,31 @@ def test_generic_rates_use_the_generic_path(pkg):
     eng.close()
 
 
+@pytest.mark.parametrize("coherent_ms,fft_len", [(1, 8192), (2, 16384), (4, 32768)])
+def test_power_of_two_rate_runs_the_circular_transform(pkg, coherent_ms, fft_len):
+    # 8.192 MHz: n_coh = 8192 * coherent_ms is a power of two, so the reference's n_coh-point
+    # circular correlation is the M = n_coh transform itself (no extension; L = 2 at 32768)
+    fs = 8.192e6
+    cfg = pkg.AcqConfig(doppler_min_hz=-1000.0, doppler_max_hz=1000.0, doppler_step_hz=250.0,
+                        coherent_ms=coherent_ms, noncoherent_rounds=2)
+    ocfg = oracle.OracleConfig(doppler_min_hz=-1000.0, doppler_max_hz=1000.0, doppler_step_hz=250.0,
+                               coherent_ms=coherent_ms, noncoherent_rounds=2)
+    x = oracle.synthesize_signal(7, 430.0, 2222, 0.3, fs, 2 * coherent_ms * 1e-3,
+                                 oracle.sigma_for_cn0_dbhz(44.0, fs), 77)
+    prns = [7, 12, 30]
+    eng = pkg.AcqEngine(fs, prns, cfg)
+    assert eng.info["path"] == 4 and eng.info["fft_len"] == fft_len
+    res = eng.search(x).results()[0]
+    assert res[0].detected and res[0].code_phase_samples == 2222
+    for g, prn in zip(res, prns):
+        r = oracle.acquire_channel(x, fs, prn, ocfg, want_map=True)
+        gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples, peak_metric=g.peak_metric,
+                  detected=g.detected)
+        verdict = compare(gd, r, ocfg.detection_threshold, r["power_map"], ocfg.doppler_bins_hz())
+        assert verdict in ("exact", "tie"), f"{coherent_ms} ms prn {prn}: {verdict}"
+    eng.close()
+
+
 @pytest.mark.parametrize("n_snap", [1, 3, 17, 40])
 def test_chunked_staging_matches_device_resident(pkg, n_snap):
     # a small spectrum scratch forces many compute chunks (a short first one, then full ones)
