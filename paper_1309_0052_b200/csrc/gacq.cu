@@ -386,11 +386,14 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         const int gen_l = c->logM > kGenMaxLogM ? 2 : 1;
         const int gen_pts = (1 << c->logM) / gen_l;
         const int gen_smem = (int)sizeof(float2) * (GACQ_GEN_STOCKHAM ? gen_pts + gen_pts / 16 : gen_pts);
+        const bool gen_v16 = gen_vpt(c->logM - (gen_l == 2)) == 16;
         if (c->gen) {
             if (gen_l == 2)
-                gacq_gen_fwd_kernel<2><<<(unsigned)(np * c->R * 2), kGenThreads, gen_smem, c->stream>>>(ga);
+                gacq_gen_fwd_kernel<2, 32><<<(unsigned)(np * c->R * 2), kGenThreads, gen_smem, c->stream>>>(ga);
+            else if (gen_v16)
+                gacq_gen_fwd_kernel<1, 16><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
             else
-                gacq_gen_fwd_kernel<1><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
+                gacq_gen_fwd_kernel<1, 32><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
         } else if (c->pfa) {
             FwdPfaArgs fa{in, in_stride, c->d_carrier, Zp, p0, c->B, c->R, c->n_coh, c->P, c->K};
@@ -403,10 +406,13 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (!c->gen) CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
         if (c->gen) {
+            const int cs = gen_corr_smem(c->logM, c->P);
             if (gen_l == 2)
-                gacq_gen_corr_kernel<2><<<(unsigned)(np * c->n_prn), kGenThreads, gen_smem, c->stream>>>(ga);
+                gacq_gen_corr_kernel<2, 32><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
+            else if (gen_v16)
+                gacq_gen_corr_kernel<1, 16><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
             else
-                gacq_gen_corr_kernel<1><<<(unsigned)(np * c->n_prn), kGenThreads, gen_smem, c->stream>>>(ga);
+                gacq_gen_corr_kernel<1, 32><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
         } else if (c->pfa) {
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
@@ -739,14 +745,14 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaMalloc(&c->d_gtw, gtw.size() * sizeof(float2)));
         CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2)));
+        const int fwd_max = (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2);
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
+        const int corr1_max = gen_corr_smem(kGenMaxLogM, kGenMaxM / 2);
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, corr1_max));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, corr1_max));
+        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
     }
     const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * (c->pfa ? kBuf : kM)) *
                                (int64_t)sizeof(float2);

@@ -40,6 +40,11 @@ constexpr int kGenThreads = 512;  // kGenMaxM = 32 * kGenThreads (gen_fft_stockh
 #ifndef GACQ_GEN_STOCKHAM
 #define GACQ_GEN_STOCKHAM 1  // register-radix Stockham passes (0: in-place radix-4 DIT from bit-reversed input)
 #endif
+// corr kernel dynamic smem: padded transform buffer of M / L points, plus P floats when L = 1
+inline int gen_corr_smem(int logM, int P) {
+    const int L = logM > kGenMaxLogM ? 2 : 1, pts = (1 << logM) / L;
+    return (int)sizeof(float2) * (GACQ_GEN_STOCKHAM ? pts + pts / 16 : pts) + (L == 1 ? 4 * P : 0);
+}
 
 // In-place DFT of x[0, 2^logM) held in bit-reversed order, natural order out.
 // tw[e * tw_stride] = (cos, sin)(2 pi e / 2^logM), e < 2^logM / 2; S = -1 forward, +1 inverse
@@ -118,10 +123,10 @@ __device__ __forceinline__ void gen_dft(cx (&v)[R]) {
 // x[16 j' + r] would otherwise put a warp's 32 stores into one bank group)
 __device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
 
-template <int S, int R>
+template <int S, int R, int VPT>
 __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs, int logNs,
                                                   const float2* __restrict__ tw, int L) {
-    constexpr int kGroups = 32 / R;  // 32 values per thread at Ms = 32 * blockDim
+    constexpr int kGroups = VPT / R;  // VPT values per thread (Ms <= VPT * blockDim)
     constexpr int kLogR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const int Ms = 1 << logMs, ng = Ms >> kLogR, Ns = 1 << logNs;
     const int tw_step = L << (logMs - logNs - kLogR);  // W_(Ns R) in units of W_M
@@ -171,16 +176,20 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs,
 }
 
 // In-place natural-order DFT of x[0, 2^logMs) (sign S, unnormalised): radix-16 passes, then
-// one radix-8/4/2 pass for the remaining bits. Needs 2^logMs <= 32 * blockDim.
-template <int S>
+// one radix-8/4/2 pass for the remaining bits. Needs 2^logMs <= VPT * blockDim; VPT = 16 halves
+// the values each thread holds across a pass's barrier (no spills at 128 registers).
+template <int S, int VPT>
 __device__ __forceinline__ void gen_fft_stockham(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, int L) {
     int logNs = 0;
-    for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16>(x, logMs, logNs, tw, L);
+    for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16, VPT>(x, logMs, logNs, tw, L);
     const int rem = logMs - logNs;
-    if (rem == 3) gen_stockham_pass<S, 8>(x, logMs, logNs, tw, L);
-    else if (rem == 2) gen_stockham_pass<S, 4>(x, logMs, logNs, tw, L);
-    else if (rem == 1) gen_stockham_pass<S, 2>(x, logMs, logNs, tw, L);
+    if (rem == 3) gen_stockham_pass<S, 8, VPT>(x, logMs, logNs, tw, L);
+    else if (rem == 2) gen_stockham_pass<S, 4, VPT>(x, logMs, logNs, tw, L);
+    else if (rem == 1) gen_stockham_pass<S, 2, VPT>(x, logMs, logNs, tw, L);
 }
+// values per thread of a transform of 2^logMs points on kGenThreads threads
+constexpr int gen_vpt(int logMs) { return (1 << logMs) <= 16 * 512 ? 16 : 32; }
+
 
 
 struct GenArgs {
@@ -197,8 +206,9 @@ struct GenArgs {
 };
 
 
-// grid: pairs_in_chunk * R * L CTAs of kGenThreads; dynamic smem (M / L) * 8 bytes
-template <int L>
+// grid: pairs_in_chunk * R * L CTAs of kGenThreads; dynamic smem (M / L) * 8 bytes;
+// VPT = gen_vpt(logM - (L == 2))
+template <int L, int VPT>
 __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a) {
     extern __shared__ __align__(16) cx sm[];
     const int M = 1 << a.logM, Ms = M / L, logMs = a.logM - (L == 2), N = a.n_coh;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
     }
     __syncthreads();
 #if GACQ_GEN_STOCKHAM
-    gen_fft_stockham<-1>(sm, logMs, a.tw, L);
+    gen_fft_stockham<-1, VPT>(sm, logMs, a.tw, L);
 #else
     gen_fft_inplace<-1>(sm, logMs, a.tw, L);
 #endif
@@ -235,8 +245,10 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
 }
 
 // grid: pairs_in_chunk * n_prn CTAs of kGenThreads (item = lp * n_prn + pi);
-// dynamic smem (M / L) * 8 bytes
-template <int L>
+// dynamic smem: the transform buffer (M / L) * 8 bytes (padded), then for L = 1 the P float
+// power accumulators (shared memory rather than registers: live across the transform they
+// would push the 512-thread CTA past its 128 registers -- gen_corr_smem)
+template <int L, int VPT>
 __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a) {
     extern __shared__ __align__(16) cx sm[];
     __shared__ float red_v[kGenThreads / 32], red_f[kGenThreads / 32];
@@ -245,10 +257,15 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     const int M = 1 << a.logM, Ms = M / L, logMs = a.logM - (L == 2);
     const int lp = blockIdx.x / a.n_prn, pi = blockIdx.x % a.n_prn;
     const cx* cg = a.Cg + (int64_t)pi * M;
-    float acc[kPer];
+    constexpr bool kSmemAcc = L == 1;
+    float acc[kSmemAcc ? 1 : kPer];
+    float* accs = reinterpret_cast<float*>(sm + (GACQ_GEN_STOCKHAM ? Ms + Ms / 16 : Ms));
+    // power accumulator of this thread's lag i (t = threadIdx.x + i kGenThreads < P)
+    auto A = [&](int i) -> float& { return kSmemAcc ? accs[threadIdx.x + i * kGenThreads] : acc[i]; };
     cx e0[L == 2 ? kPer : 1];  // E_0 of this thread's lags while E_1 is computed
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) acc[i] = 0.f;
+    for (int i = 0; i < kPer; ++i)
+        if (!kSmemAcc || threadIdx.x + i * kGenThreads < a.P) A(i) = 0.f;
     for (int rd = 0; rd < a.R; ++rd) {
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M;
 #pragma unroll
@@ -258,10 +275,27 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
                 sm[GACQ_GEN_STOCKHAM ? gpad(k) : bitrev(k, logMs)] = cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
             __syncthreads();
 #if GACQ_GEN_STOCKHAM
-            gen_fft_stockham<1>(sm, logMs, a.tw, L);
+            gen_fft_stockham<1, VPT>(sm, logMs, a.tw, L);
 #else
             gen_fft_inplace<1>(sm, logMs, a.tw, L);
 #endif
+            if (kSmemAcc) {
+                // lag t = tid + i kGenThreads sits at sb[i kSt] (gpad(tid + 512 i) = gpad(tid) + 544 i):
+                // one base address instead of kPer, which would stay live across the transform
+                constexpr int kSt = GACQ_GEN_STOCKHAM ? kGenThreads + kGenThreads / 16 : kGenThreads;
+                const cx* sb = sm + (GACQ_GEN_STOCKHAM ? gpad(threadIdx.x) : threadIdx.x);
+                float* ab = accs + threadIdx.x;
+                const int nl = (a.P - (int)threadIdx.x + kGenThreads - 1) / kGenThreads;
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    if (i < nl) {
+                        const cx v = sb[i * kSt];
+                        ab[i * kGenThreads] = fmaf(im(v), im(v), fmaf(re(v), re(v), ab[i * kGenThreads]));
+                    }
+                }
+                __syncthreads();
+                continue;
+            }
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const int t = threadIdx.x + i * kGenThreads;
@@ -272,7 +306,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
                         continue;
                     }
                     if (L == 2) v = add2(e0[i], cmul(v, gen_tw<1>(a.tw, t, M)));  // E_0 + W_M^t E_1
-                    acc[i] = fmaf(im(v), im(v), fmaf(re(v), re(v), acc[i]));  // acquisition.py:149
+                    A(i) = fmaf(im(v), im(v), fmaf(re(v), re(v), A(i)));  // acquisition.py:149
                 }
             }
             __syncthreads();
@@ -285,7 +319,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
         const int t = threadIdx.x + i * kGenThreads;
-        if (t < a.P && better(acc[i], t, best, bidx)) { best = acc[i]; bidx = t; }
+        if (t < a.P && better(A(i), t, best, bidx)) { best = A(i); bidx = t; }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -310,8 +344,8 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
         if (t < a.P) {
             int d = abs(t - bidx);
             d = min(d, a.P - d);
-            if (d > a.radius) fl = fmaxf(fl, acc[i]);  // acquisition.py:155-159
-            if (pm) pm[t] = acc[i];
+            if (d > a.radius) fl = fmaxf(fl, A(i));  // acquisition.py:155-159
+            if (pm) pm[t] = A(i);
         }
     }
 #pragma unroll
