@@ -1048,7 +1048,7 @@ int gacq_trk_create(gacq_trk** out, int32_t device) {
     cudaError_t e;
     if ((e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(gacq_epl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kTrkMaxSmem)) != cudaSuccess ||
+                                  kEplSmem)) != cudaSuccess ||
         (e = cudaMalloc(&t->d_chips, chips.size())) != cudaSuccess ||
         (e = cudaMemcpy(t->d_chips, chips.data(), chips.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
         trk_free(t);
@@ -1160,9 +1160,6 @@ int gacq_trk_epl(gacq_trk* t, const void* blocks, int64_t total, int32_t n, cons
                  int64_t n_chan, uint32_t flags, float* out) {
     if (!t || !blocks || !chans || !out) return fail(GACQ_ERR_INVALID, "null argument");
     if (n < 1 || n_chan < 1 || total < n) return fail(GACQ_ERR_INVALID, "bad sizes");
-    const int smem = n * (int)(sizeof(float2) + 3);
-    if (smem > kTrkMaxSmem)
-        return fail(GACQ_ERR_UNSUPPORTED, "tracking block of %d samples exceeds one CTA's shared memory", n);
     for (int64_t i = 0; i < n_chan; ++i) {
         if (chans[i].prn < 1 || chans[i].prn > 32)
             return fail(GACQ_ERR_INVALID, "prn must be an integer in 1..32, got %d", chans[i].prn);
@@ -1171,6 +1168,10 @@ int gacq_trk_epl(gacq_trk* t, const void* blocks, int64_t total, int32_t n, cons
         if (chans[i].carrier_p0 >> 48 || chans[i].carrier_step >> 48 || chans[i].code_step >= kCodeMod ||
             chans[i].code_p0[0] >= kCodeMod || chans[i].code_p0[1] >= kCodeMod || chans[i].code_p0[2] >= kCodeMod)
             return fail(GACQ_ERR_INVALID, "channel %lld NCO word out of range", (long long)i);
+        // the kernel evaluates the code NCO statelessly as p0 + k step in 64 bits
+        if (chans[i].code_step && (uint64_t)(n - 1) > (~0ull - kCodeMod) / chans[i].code_step)
+            return fail(GACQ_ERR_UNSUPPORTED, "channel %lld: %d samples at code step %llu overflow the 64-bit code NCO",
+                        (long long)i, n, (unsigned long long)chans[i].code_step);
     }
     std::lock_guard<std::mutex> lk(t->mu);
     DeviceGuard g(t->device);
@@ -1184,8 +1185,8 @@ int gacq_trk_epl(gacq_trk* t, const void* blocks, int64_t total, int32_t n, cons
     if ((rc = grow(&t->d_chans, &t->chans_cap, n_chan))) return rc;
     if ((rc = grow(&t->d_out, &t->out_cap, n_chan * 6))) return rc;
     CUDA_TRY(cudaMemcpyAsync(t->d_chans, chans, n_chan * sizeof(gacq_epl_chan), cudaMemcpyHostToDevice, t->stream));
-    gacq_epl_kernel<<<(unsigned)n_chan, kTrkThreads, smem, t->stream>>>(reinterpret_cast<const cx*>(x), n,
-                                                                          t->d_chans, t->d_chips, t->d_out);
+    gacq_epl_kernel<<<(unsigned)((n_chan + kEplChans - 1) / kEplChans), kEplThreads, kEplSmem, t->stream>>>(
+        reinterpret_cast<const cx*>(x), n, t->d_chans, n_chan, t->d_chips, t->d_out);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out, t->d_out, n_chan * 6 * sizeof(float), cudaMemcpyDeviceToHost, t->stream));
     CUDA_TRY(cudaStreamSynchronize(t->stream));
