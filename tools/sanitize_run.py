@@ -4,8 +4,8 @@
 
 Exercises every device kernel: the table builders, the 1023-point path (K1/K2 at D = 2, 4, 16,
 powers in registers and in L2 rows), the 2048-point path (GACQ_PATH=2048), the tensor-core K2
-(GACQ_TC=1), the generic power-of-two path (5 MHz, and 6 MHz x 2 ms for the two-part
-transform), K3, the power-map hook, the int8 dequantizer and the tracking correlators.
+(GACQ_TC=1), the generic power-of-two path (5 MHz; 6 MHz x 2 ms for the two-part transform;
+8.192 MHz at 1 and 4 ms for the circular transforms), K3, the power-map hook, the int8 dequantizer and the tracking correlators.
 """
 
 import os
@@ -47,12 +47,19 @@ def main():
     run(16.368e6, 1, env={"GACQ_TC": "1"})
     run(5.0e6, 2)
     run(6.0e6, 1, coh=2)
+    run(8.192e6, 2)  # power-of-two n_coh: circular 8192-point transform, 16 values per thread
+    run(8.192e6, 1, coh=4)  # circular 32768-point (two-part) transform
     os.environ.pop("GACQ_TC", None)
     st = [trk.TrackState(prn=p, code_phase_chips=10.0 * p, carrier_phase_cycles=0.0, doppler_hz=100.0 * p,
                          code_rate_hz=1.023e6, sample_rate_hz=4.092e6) for p in (1, 2, 3)]
     blk = oracle.make_snapshot(0, 4.092e6, 1e-3, base_seed=3)[0]
     s2, out = trk.track_epoch_batch(blk, [0, 0, 0], st, trk.TrackConfig())
     print("track", [round(o.ip, 2) for o in out])
+    # 40 channels: a full 32-channel CTA and a partial one
+    st = [trk.TrackState(prn=1 + i % 32, code_phase_chips=7.0 * i, carrier_phase_cycles=0.1, doppler_hz=50.0 * i,
+                         code_rate_hz=1.023e6, sample_rate_hz=4.092e6) for i in range(40)]
+    s2, out = trk.track_epoch_batch(blk, [0] * 40, st, trk.TrackConfig())
+    print("track40", round(out[39].ip, 2))
 
 
 if __name__ == "__main__":
