@@ -229,6 +229,18 @@ int gacq_trk_close(const float* sums, const gacq_trk_batch* batch, const gacq_tr
 int gacq_trk_chans(const gacq_trk_batch* batch, const gacq_trk_config* cfg, const int64_t* offsets,
                    gacq_epl_chan* chans);
 
+/* One tracking epoch of a whole batch in one call: gacq_trk_chans + gacq_trk_epl + gacq_trk_close
+ * (tracking.py:126-275 for every channel), pipelined over channel slices so that one slice's
+ * correlator kernel runs while the host computes the next slices' NCO words and closes the
+ * previous ones. The block length is round(sample_rate_hz[0] * integration_ms / 1000). Results
+ * are those of the three calls: sums[c*6 + 0..5] the correlators, out[c*3 + 0..2] as
+ * gacq_trk_close, the batch advanced in place. On a degenerate channel (*bad_channel = its
+ * index, GACQ_ERR_INVALID) the batch may already be partly advanced: pass a copy (the Python
+ * track_step does). Replaces the per-epoch loop of tracking.py:226-275 over channels. */
+int gacq_trk_step(gacq_trk* trk, const void* blocks, int64_t total_samples, const int64_t* offsets,
+                  gacq_trk_batch* batch, const gacq_trk_config* cfg, uint32_t flags, float* sums, double* out,
+                  int64_t* bad_channel);
+
 /* Page-locked host buffers for overlapped H2D (cudaHostAlloc / cudaFreeHost). */
 int gacq_host_alloc(int64_t bytes, void** out);
 int gacq_host_free(void* ptr);

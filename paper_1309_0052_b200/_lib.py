@@ -67,7 +67,7 @@ ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
 EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
            "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
            "gacq_host_alloc", "gacq_host_free", "gacq_ca_code", "gacq_trk_create", "gacq_trk_destroy",
-           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth", "gacq_trk_close", "gacq_trk_chans")
+           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth", "gacq_trk_close", "gacq_trk_chans", "gacq_trk_step")
 FMT_INT8, FMT_INT16 = 0, 1
 
 
@@ -90,6 +90,8 @@ def _load() -> C.CDLL:
     lib.gacq_trk_close.argtypes = [C.c_void_p, C.POINTER(TrkBatch), C.POINTER(TrkConfig), C.c_void_p,
                                    C.POINTER(C.c_int64)]
     lib.gacq_trk_chans.argtypes = [C.POINTER(TrkBatch), C.POINTER(TrkConfig), C.c_void_p, C.c_void_p]
+    lib.gacq_trk_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(TrkBatch),
+                                  C.POINTER(TrkConfig), C.c_uint32, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
     lib.gacq_synth.argtypes = [C.c_int32, C.c_double, C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_double,
                                C.c_uint64, C.c_void_p]
     lib.gacq_stats_get.argtypes = [C.c_void_p, C.POINTER(Stats)]

@@ -1015,6 +1015,10 @@ struct gacq_trk {
     int64_t chans_cap = 0;
     float* d_out = nullptr;
     int64_t out_cap = 0;
+    gacq_epl_chan* h_chans = nullptr;  // page-locked staging of gacq_trk_step
+    float* h_sums = nullptr;
+    int64_t h_cap = 0;                 // channels
+    std::vector<cudaEvent_t> slice_events;
 };
 
 static void trk_free(gacq_trk* t) {
@@ -1026,6 +1030,9 @@ static void trk_free(gacq_trk* t) {
         cudaFree(t->d_blocks);
         cudaFree(t->d_chans);
         cudaFree(t->d_out);
+        cudaFreeHost(t->h_chans);
+        cudaFreeHost(t->h_sums);
+        for (cudaEvent_t e : t->slice_events) cudaEventDestroy(e);
         if (t->stream) cudaStreamDestroy(t->stream);
     }
     delete t;
@@ -1060,89 +1067,94 @@ int gacq_trk_create(gacq_trk** out, int32_t device) {
 
 void gacq_trk_destroy(gacq_trk* t) { trk_free(t); }
 
-int gacq_trk_close(const float* sums, const gacq_trk_batch* b, const gacq_trk_config* cfg, double* out,
-                   int64_t* bad) {
-    using gtrk::carrier_phase_fixed; using gtrk::carrier_step_fixed; using gtrk::code_phase_fixed;
-    using gtrk::code_step_fixed; using gtrk::py_fmod; using gtrk::rint64; using gtrk::parallel_for;
-    if (!sums || !b || !cfg || !out) return fail(GACQ_ERR_INVALID, "null argument");
-    if (b->n < 1) return fail(GACQ_ERR_INVALID, "no channels");
-    const double sp = cfg->correlator_spacing_chips;
-    const double t = cfg->integration_ms * 1e-3;
-    const int64_t n = rint64(b->sample_rate_hz[0] * cfg->integration_ms * 1e-3);  // tracking.py:122-123
-    auto gains = [](double bw, double* g1, double* g2) {  // tracking.py:188-190
-        const double w0 = bw / 0.53;
-        *g1 = 2.0 * gtrk::kLoopDamping * w0;
-        *g2 = w0 * w0;
-    };
-    double g1p, g2p, g1d, g2d;
-    gains(cfg->pll_bandwidth_hz, &g1p, &g2p);
-    gains(cfg->dll_bandwidth_hz, &g1d, &g2d);
-    const double two_pi = 2.0 * 3.141592653589793;
-    const double alpha = 1.0 / gtrk::kLockSmoothing;
+}  // extern "C"
+
+namespace gtrk {
+
+// tracking.py:168-275 for channels [a, e) of a batch, in place (see gacq_trk_close)
+struct Closure {
+    const gacq_trk_config* cfg;
+    double sp, t, g1p, g2p, g1d, g2d, alpha;
+    int64_t n;
+    Closure(const gacq_trk_batch* b, const gacq_trk_config* c) : cfg(c) {
+        sp = c->correlator_spacing_chips;
+        t = c->integration_ms * 1e-3;
+        n = rint64(b->sample_rate_hz[0] * c->integration_ms * 1e-3);  // tracking.py:122-123
+        auto gains = [](double bw, double* g1, double* g2) {  // tracking.py:188-190
+            const double w0 = bw / 0.53;
+            *g1 = 2.0 * kLoopDamping * w0;
+            *g2 = w0 * w0;
+        };
+        gains(c->pll_bandwidth_hz, &g1p, &g2p);
+        gains(c->dll_bandwidth_hz, &g1d, &g2d);
+        alpha = 1.0 / kLockSmoothing;
+    }
     // degenerate channels first (the reference raises before touching any state): a zero
     // prompt correlator fails the PLL discriminator (tracking.py:181-182), and with zero early
-    // and late as well the DLL one first (tracking.py:173-175)
-    for (int64_t i = 0; i < b->n; ++i) {
-        const float* s = sums + 6 * i;
-        if (s[2] == 0.f && s[3] == 0.f) {
-            if (bad) *bad = i;
-            const bool all = s[0] == 0.f && s[1] == 0.f && s[4] == 0.f && s[5] == 0.f;
-            return fail(GACQ_ERR_INVALID, "%s on channel %lld", all ? "all correlators zero" : "prompt correlator is zero",
-                        (long long)i);
-        }
-    }
-    parallel_for(b->n, [&](int64_t a, int64_t e_) {
-        for (int64_t i = a; i < e_; ++i) {
+    // and late as well the DLL one first (tracking.py:173-175). Returns the first bad index or -1.
+    static int64_t first_degenerate(const float* sums, int64_t a, int64_t e, bool* all) {
+        for (int64_t i = a; i < e; ++i) {
             const float* s = sums + 6 * i;
-            const double ie = s[0], qe = s[1], ip = s[2], qp = s[3], il = s[4], ql = s[5];
-            const double e = ie * ie + qe * qe, l = il * il + ql * ql;  // tracking.py:170-171
-            const double ed = e + l == 0 ? 0.0 : (e - l) / (e + l) * (1.0 - sp / 2.0) / 2.0;
-            const double ep = ip == 0.0 ? std::copysign(0.25, qp) : std::atan(qp / ip) / two_pi;  // :179-185
-            const double fs = b->sample_rate_hz[i];
-            const double pll_acc = b->pll_acc[i] + g2p * t * (ep + b->pll_prev[i]) / 2.0;  // :198-200
-            const double dll_acc = b->dll_acc[i] + g2d * t * (ed + b->dll_prev[i]) / 2.0;
-            const double doppler = b->doppler_hz[i] + (pll_acc - b->pll_acc[i]);  // :242
-            const double code_rate = gtrk::kChipRate * (1.0 + doppler / gtrk::kL1) + dll_acc;  // :243
-            const uint64_t pc = (carrier_phase_fixed(b->carrier_phase_cycles[i]) +
-                                 (uint64_t)n * carrier_step_fixed(b->doppler_hz[i], fs) +
-                                 carrier_phase_fixed(t * g1p * ep)) % (uint64_t)gtrk::kCarrierScale;  // :211-215
-            const uint64_t nudge = (uint64_t)rint64(py_fmod(t * g1d * ed, 1023.0) * (double)gtrk::kCodeScale);
-            const uint64_t pcode = (code_phase_fixed(b->code_phase_chips[i]) +
-                                    (uint64_t)n * code_step_fixed(b->code_rate_hz[i], fs) + nudge) %
-                                   (uint64_t)gtrk::kCodeModulus;  // :218-223
-            const double nbd = ip * ip - qp * qp, nbp = ip * ip + qp * qp;  // :252-260
-            double nbd_s = nbd, nbp_s = nbp;
-            if (b->epoch[i] != 0) {
-                nbd_s = b->lock_nbd[i] + alpha * (nbd - b->lock_nbd[i]);
-                nbp_s = b->lock_nbp[i] + alpha * (nbp - b->lock_nbp[i]);
+            if (s[2] == 0.f && s[3] == 0.f) {
+                *all = s[0] == 0.f && s[1] == 0.f && s[4] == 0.f && s[5] == 0.f;
+                return i;
             }
-            out[3 * i + 0] = ed;
-            out[3 * i + 1] = ep;
-            out[3 * i + 2] = nbp_s > 0 ? nbd_s / nbp_s : 0.0;
-            b->code_phase_chips[i] = (double)pcode / (double)gtrk::kCodeScale;
-            b->carrier_phase_cycles[i] = (double)pc / (double)gtrk::kCarrierScale;
-            b->doppler_hz[i] = doppler;
-            b->code_rate_hz[i] = code_rate;
-            b->dll_acc[i] = dll_acc;
-            b->dll_prev[i] = ed;
-            b->pll_acc[i] = pll_acc;
-            b->pll_prev[i] = ep;
-            b->lock_nbd[i] = nbd_s;
-            b->lock_nbp[i] = nbp_s;
-            b->epoch[i] += 1;
         }
-    });
-    return GACQ_OK;
-}
+        return -1;
+    }
+    void range(const float* sums, const gacq_trk_batch* b, double* out, int64_t a0, int64_t e0) const {
+        const double two_pi = 2.0 * 3.141592653589793;
+        parallel_for(e0 - a0, [&](int64_t ra, int64_t re_) {
+            for (int64_t i = a0 + ra; i < a0 + re_; ++i) {
+                const float* s = sums + 6 * i;
+                const double ie = s[0], qe = s[1], ip = s[2], qp = s[3], il = s[4], ql = s[5];
+                const double e = ie * ie + qe * qe, l = il * il + ql * ql;  // tracking.py:170-171
+                const double ed = e + l == 0 ? 0.0 : (e - l) / (e + l) * (1.0 - sp / 2.0) / 2.0;
+                const double ep = ip == 0.0 ? std::copysign(0.25, qp) : std::atan(qp / ip) / two_pi;  // :179-185
+                const double fs = b->sample_rate_hz[i];
+                const double pll_acc = b->pll_acc[i] + g2p * t * (ep + b->pll_prev[i]) / 2.0;  // :198-200
+                const double dll_acc = b->dll_acc[i] + g2d * t * (ed + b->dll_prev[i]) / 2.0;
+                const double doppler = b->doppler_hz[i] + (pll_acc - b->pll_acc[i]);  // :242
+                const double code_rate = kChipRate * (1.0 + doppler / kL1) + dll_acc;  // :243
+                const uint64_t pc = (carrier_phase_fixed(b->carrier_phase_cycles[i]) +
+                                     (uint64_t)n * carrier_step_fixed(b->doppler_hz[i], fs) +
+                                     carrier_phase_fixed(t * g1p * ep)) % (uint64_t)kCarrierScale;  // :211-215
+                const uint64_t nudge = (uint64_t)rint64(py_fmod(t * g1d * ed, 1023.0) * (double)kCodeScale);
+                const uint64_t pcode = (code_phase_fixed(b->code_phase_chips[i]) +
+                                        (uint64_t)n * code_step_fixed(b->code_rate_hz[i], fs) + nudge) %
+                                       (uint64_t)kCodeModulus;  // :218-223
+                const double nbd = ip * ip - qp * qp, nbp = ip * ip + qp * qp;  // :252-260
+                double nbd_s = nbd, nbp_s = nbp;
+                if (b->epoch[i] != 0) {
+                    nbd_s = b->lock_nbd[i] + alpha * (nbd - b->lock_nbd[i]);
+                    nbp_s = b->lock_nbp[i] + alpha * (nbp - b->lock_nbp[i]);
+                }
+                out[3 * i + 0] = ed;
+                out[3 * i + 1] = ep;
+                out[3 * i + 2] = nbp_s > 0 ? nbd_s / nbp_s : 0.0;
+                b->code_phase_chips[i] = (double)pcode / (double)kCodeScale;
+                b->carrier_phase_cycles[i] = (double)pc / (double)kCarrierScale;
+                b->doppler_hz[i] = doppler;
+                b->code_rate_hz[i] = code_rate;
+                b->dll_acc[i] = dll_acc;
+                b->dll_prev[i] = ed;
+                b->pll_acc[i] = pll_acc;
+                b->pll_prev[i] = ep;
+                b->lock_nbd[i] = nbd_s;
+                b->lock_nbp[i] = nbp_s;
+                b->epoch[i] += 1;
+            }
+        });
+    }
+};
 
-int gacq_trk_chans(const gacq_trk_batch* b, const gacq_trk_config* cfg, const int64_t* offsets, gacq_epl_chan* ch) {
-    using gtrk::carrier_phase_fixed; using gtrk::carrier_step_fixed; using gtrk::code_phase_fixed;
-    using gtrk::code_step_fixed; using gtrk::py_fmod; using gtrk::rint64; using gtrk::parallel_for;
-    if (!b || !cfg || !offsets || !ch) return fail(GACQ_ERR_INVALID, "null argument");
+// gacq_epl_chan records of channels [a, e): tracking.py:126-165's NCO words (kernels.py:56-70)
+inline void chans_range(const gacq_trk_batch* b, const gacq_trk_config* cfg, const int64_t* offsets,
+                        gacq_epl_chan* ch, int64_t a0, int64_t e0) {
     const double d = cfg->correlator_spacing_chips;
     const double off[3] = {+d / 2, 0.0, -d / 2};  // tracking.py:148-156
-    parallel_for(b->n, [&](int64_t a, int64_t e_) {
-        for (int64_t i = a; i < e_; ++i) {
+    parallel_for(e0 - a0, [&](int64_t ra, int64_t re_) {
+        for (int64_t i = a0 + ra; i < a0 + re_; ++i) {
             const double fs = b->sample_rate_hz[i];
             ch[i].block_offset = offsets[i];
             ch[i].carrier_p0 = carrier_phase_fixed(b->carrier_phase_cycles[i]);
@@ -1153,6 +1165,30 @@ int gacq_trk_chans(const gacq_trk_batch* b, const gacq_trk_config* cfg, const in
             ch[i].reserved = 0;
         }
     });
+}
+
+}  // namespace gtrk
+
+extern "C" {
+
+int gacq_trk_close(const float* sums, const gacq_trk_batch* b, const gacq_trk_config* cfg, double* out,
+                   int64_t* bad) {
+    if (!sums || !b || !cfg || !out) return fail(GACQ_ERR_INVALID, "null argument");
+    if (b->n < 1) return fail(GACQ_ERR_INVALID, "no channels");
+    bool all = false;
+    const int64_t i = gtrk::Closure::first_degenerate(sums, 0, b->n, &all);
+    if (i >= 0) {
+        if (bad) *bad = i;
+        return fail(GACQ_ERR_INVALID, "%s on channel %lld", all ? "all correlators zero" : "prompt correlator is zero",
+                    (long long)i);
+    }
+    gtrk::Closure(b, cfg).range(sums, b, out, 0, b->n);
+    return GACQ_OK;
+}
+
+int gacq_trk_chans(const gacq_trk_batch* b, const gacq_trk_config* cfg, const int64_t* offsets, gacq_epl_chan* ch) {
+    if (!b || !cfg || !offsets || !ch) return fail(GACQ_ERR_INVALID, "null argument");
+    gtrk::chans_range(b, cfg, offsets, ch, 0, b->n);
     return GACQ_OK;
 }
 
@@ -1190,6 +1226,88 @@ int gacq_trk_epl(gacq_trk* t, const void* blocks, int64_t total, int32_t n, cons
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out, t->d_out, n_chan * 6 * sizeof(float), cudaMemcpyDeviceToHost, t->stream));
     CUDA_TRY(cudaStreamSynchronize(t->stream));
+    return GACQ_OK;
+}
+
+int gacq_trk_step(gacq_trk* t, const void* blocks, int64_t total, const int64_t* offsets, gacq_trk_batch* b,
+                  const gacq_trk_config* cfg, uint32_t flags, float* sums, double* out, int64_t* bad) {
+    if (!t || !blocks || !offsets || !b || !cfg || !sums || !out) return fail(GACQ_ERR_INVALID, "null argument");
+    const int64_t nch = b->n;
+    if (nch < 1) return fail(GACQ_ERR_INVALID, "no channels");
+    const int64_t n64 = gtrk::rint64(b->sample_rate_hz[0] * cfg->integration_ms * 1e-3);  // tracking.py:122-123
+    if (n64 < 1 || n64 > INT32_MAX || total < n64) return fail(GACQ_ERR_INVALID, "bad sizes");
+    const int n = (int)n64;
+    for (int64_t i = 0; i < nch; ++i) {
+        if (b->prn[i] < 1 || b->prn[i] > 32) return fail(GACQ_ERR_INVALID, "prn must be an integer in 1..32, got %d", b->prn[i]);
+        if (offsets[i] < 0 || offsets[i] + n > total)
+            return fail(GACQ_ERR_INVALID, "channel %lld block outside the sample buffer", (long long)i);
+    }
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    const float2* x = (const float2*)blocks;
+    int rc;
+    if (!(flags & GACQ_SNAPS_ON_DEVICE)) {
+        if ((rc = grow(&t->d_blocks, &t->blocks_cap, total))) return rc;
+        CUDA_TRY(cudaMemcpyAsync(t->d_blocks, blocks, total * sizeof(float2), cudaMemcpyHostToDevice, t->stream));
+        x = t->d_blocks;
+    }
+    if ((rc = grow(&t->d_chans, &t->chans_cap, nch))) return rc;
+    if ((rc = grow(&t->d_out, &t->out_cap, nch * 6))) return rc;
+    if (t->h_cap < nch) {
+        cudaFreeHost(t->h_chans);
+        cudaFreeHost(t->h_sums);
+        t->h_chans = nullptr;
+        t->h_sums = nullptr;
+        t->h_cap = 0;
+        if (cudaHostAlloc(&t->h_chans, nch * sizeof(gacq_epl_chan), cudaHostAllocDefault) != cudaSuccess ||
+            cudaHostAlloc(&t->h_sums, nch * 6 * sizeof(float), cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(GACQ_ERR_RESOURCE, "page-locked staging for %lld channels", (long long)nch);
+        }
+        t->h_cap = nch;
+    }
+    // slices of whole 32-channel CTAs, at most 4
+    const int64_t slice = std::max<int64_t>(32 * 64, ((nch + 3) / 4 + 31) / 32 * 32);
+    const int64_t n_slices = (nch + slice - 1) / slice;
+    while ((int64_t)t->slice_events.size() < n_slices) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        t->slice_events.push_back(e);
+    }
+    auto drain = [&](int r) { cudaStreamSynchronize(t->stream); return r; };
+    for (int64_t k = 0; k < n_slices; ++k) {
+        const int64_t a = k * slice, e = std::min(nch, a + slice);
+        gtrk::chans_range(b, cfg, offsets, t->h_chans, a, e);
+        for (int64_t i = a; i < e; ++i)  // the kernel evaluates the code NCO as p0 + k step in 64 bits
+            if (t->h_chans[i].code_step >= kCodeMod ||
+                (t->h_chans[i].code_step && (uint64_t)(n - 1) > (~0ull - kCodeMod) / t->h_chans[i].code_step))
+                return drain(fail(GACQ_ERR_UNSUPPORTED, "channel %lld: code NCO step out of range", (long long)i));
+        if (cudaMemcpyAsync(t->d_chans + a, t->h_chans + a, (e - a) * sizeof(gacq_epl_chan), cudaMemcpyHostToDevice,
+                            t->stream) != cudaSuccess)
+            return drain(fail(GACQ_ERR_CUDA, "chans upload: %s", cudaGetErrorString(cudaGetLastError())));
+        gacq_epl_kernel<<<(unsigned)((e - a + kEplChans - 1) / kEplChans), kEplThreads, kEplSmem, t->stream>>>(
+            reinterpret_cast<const cx*>(x), n, t->d_chans + a, e - a, t->d_chips, t->d_out + 6 * a);
+        if (cudaGetLastError() != cudaSuccess ||
+            cudaMemcpyAsync(t->h_sums + 6 * a, t->d_out + 6 * a, (e - a) * 6 * sizeof(float), cudaMemcpyDeviceToHost,
+                            t->stream) != cudaSuccess ||
+            cudaEventRecord(t->slice_events[k], t->stream) != cudaSuccess)
+            return drain(fail(GACQ_ERR_CUDA, "correlator launch failed"));
+    }
+    gtrk::Closure cl(b, cfg);
+    for (int64_t k = 0; k < n_slices; ++k) {
+        const int64_t a = k * slice, e = std::min(nch, a + slice);
+        if (cudaEventSynchronize(t->slice_events[k]) != cudaSuccess)
+            return drain(fail(GACQ_ERR_CUDA, "correlator: %s", cudaGetErrorString(cudaGetLastError())));
+        std::memcpy(sums + 6 * a, t->h_sums + 6 * a, (e - a) * 6 * sizeof(float));
+        bool all = false;
+        const int64_t i = gtrk::Closure::first_degenerate(sums, a, e, &all);
+        if (i >= 0) {
+            if (bad) *bad = i;
+            return drain(fail(GACQ_ERR_INVALID, "%s on channel %lld",
+                              all ? "all correlators zero" : "prompt correlator is zero", (long long)i));
+        }
+        cl.range(sums, b, out, a, e);
+    }
     return GACQ_OK;
 }
 

@@ -442,18 +442,36 @@ def close_loops_batch(sums: np.ndarray, batch: TrackBatch, config: TrackConfig):
 
 
 def track_step(samples, offsets, batch: TrackBatch, config: TrackConfig, device: int = 0):
-    """One epoch of a struct-of-arrays batch: one device launch + vectorised loop closure."""
+    """One epoch of a struct-of-arrays batch in one native call (libgacq gacq_trk_step): the NCO
+    words, the correlator kernel and the loop closure of tracking.py:126-275 for every channel,
+    pipelined over channel slices. Returns (new batch, outputs dict) like close_loops_batch; the
+    input batch is not modified (a degenerate channel raises before anything is returned)."""
     eng = get_track_engine(device)
     b = _owned(batch)
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     if off.shape != (b.prn.size,):
         raise InvalidInputError("one block offset per channel")
-    chans, sums = eng.pinned(b.prn.size)  # page-locked: the per-epoch H2D / D2H run at full speed
+    cai = getattr(samples, "__cuda_array_interface__", None)
+    if cai is not None:
+        if cai["typestr"] != "<c8":
+            raise InvalidInputError("device samples must be complex64")
+        total, ptr, flags = int(np.prod(cai["shape"])), cai["data"][0], _lib.SNAPS_ON_DEVICE
+    else:
+        arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
+        total, ptr, flags = arr.size, arr.ctypes.data, 0
+    sums = np.empty((b.prn.size, 6), dtype=np.float32)
+    out = np.empty((b.prn.size, 3), dtype=np.float64)
+    bad = C.c_int64(-1)
     cb, cc = _c_batch(b), _c_config(config)
-    _lib.check(_lib.lib.gacq_trk_chans(C.byref(cb), C.byref(cc), off.ctypes.data, chans.ctypes.data))
-    n = round(float(b.sample_rate_hz[0]) * config.integration_ms * 1e-3)
-    eng.correlate_chans(samples, chans, n, out=sums)
-    return close_loops_batch(sums, b, config)
+    rc = _lib.lib.gacq_trk_step(eng._trk, ptr, total, off.ctypes.data, C.byref(cb), C.byref(cc), flags,
+                                sums.ctypes.data, out.ctypes.data, C.byref(bad))
+    if rc == _lib.ERR_INVALID and bad.value >= 0:
+        raise DegenerateInputError((_lib.lib.gacq_last_error() or b"").decode())
+    _lib.check(rc)
+    s64 = sums.astype(np.float64)
+    outs = dict(ie=s64[:, 0], qe=s64[:, 1], ip=s64[:, 2], qp=s64[:, 3], il=s64[:, 4], ql=s64[:, 5],
+                dll_error_chips=out[:, 0], pll_error_cycles=out[:, 1], lock_metric=out[:, 2])
+    return b, outs
 
 
 def track_epoch_batch(samples, offsets, states, config: TrackConfig, device: int = 0):

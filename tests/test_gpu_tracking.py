@@ -141,3 +141,53 @@ def test_tracking_api_semantics(trk):
     zero = np.zeros(8184, np.complex64)
     with pytest.raises(trk.DegenerateInputError):
         trk.track_epoch(zero, st, trk.TrackConfig())
+
+
+def test_track_step_slices_equal_separate_calls(trk):
+    """gacq_trk_step pipelines > 2048 channels over several slices (kernel of one slice under the
+    host work of the others); results equal the three separate calls (NCO words, correlators,
+    closure) bit for bit, and the input batch is left untouched."""
+    import dataclasses
+
+    import torch
+
+    c = case("chain_c3_snap0")
+    bl = blocks(c)
+    cfg = trk.TrackConfig(**c["config"])
+    n = bl[0].size
+    dev = torch.from_numpy(np.concatenate(bl[:2])).cuda()
+    base = [to_state(trk, ch["init"]) for ch in c["channels"]]
+    states = [dataclasses.replace(base[i % len(base)], doppler_hz=base[i % len(base)].doppler_hz + 0.5 * (i // len(base)))
+              for i in range(5000)]
+    batch = trk.TrackBatch.from_states(states)
+    before = batch.doppler_hz.copy()
+    offs = np.array([(i % 2) * n for i in range(5000)], dtype=np.int64)
+    b1, o1 = trk.track_step(dev, offs, batch, cfg)
+    np.testing.assert_array_equal(batch.doppler_hz, before)
+    eng = trk.get_track_engine(0)
+    sums = eng.correlate_chans(dev, trk.epl_chans(batch, offs, cfg), n)
+    b2, o2 = trk.close_loops_batch(sums, batch, cfg)
+    for k in o1:
+        np.testing.assert_array_equal(o1[k], o2[k], err_msg=k)
+    for f in ("code_phase_chips", "carrier_phase_cycles", "doppler_hz", "code_rate_hz", "pll_acc", "lock_nbp"):
+        np.testing.assert_array_equal(getattr(b1, f), getattr(b2, f), err_msg=f)
+
+
+def test_track_step_degenerate_channel_in_a_later_slice(trk):
+    """A channel whose block is all zeros raises DegenerateInputError naming it (tracking.py:173-175),
+    even when earlier slices were already closed; the caller's batch is unchanged."""
+    import torch
+
+    c = case("chain_c3_snap0")
+    bl = blocks(c)
+    cfg = trk.TrackConfig(**c["config"])
+    n = bl[0].size
+    dev = torch.from_numpy(np.concatenate([bl[0], np.zeros(n, np.complex64)])).cuda()
+    base = [to_state(trk, ch["init"]) for ch in c["channels"]]
+    batch = trk.TrackBatch.from_states([base[i % len(base)] for i in range(4100)])
+    before = batch.code_phase_chips.copy()
+    offs = np.zeros(4100, dtype=np.int64)
+    offs[4099] = n
+    with pytest.raises(trk.DegenerateInputError, match="all correlators zero on channel 4099"):
+        trk.track_step(dev, offs, batch, cfg)
+    np.testing.assert_array_equal(batch.code_phase_chips, before)
