@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
 #else
             gen_fft_inplace<1>(sm, logMs, a.tw, L);
 #endif
-            if (kSmemAcc) {
+            if constexpr (kSmemAcc) {
                 // lag t = tid + i kGenThreads sits at sb[i kSt] (gpad(tid + 512 i) = gpad(tid) + 544 i):
                 // one base address instead of kPer, which would stay live across the transform
                 constexpr int kSt = GACQ_GEN_STOCKHAM ? kGenThreads + kGenThreads / 16 : kGenThreads;
@@ -293,9 +293,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
                         ab[i * kGenThreads] = fmaf(im(v), im(v), fmaf(re(v), re(v), ab[i * kGenThreads]));
                     }
                 }
-                __syncthreads();
-                continue;
-            }
+            } else {
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const int t = threadIdx.x + i * kGenThreads;
@@ -308,6 +306,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
                     if (L == 2) v = add2(e0[i], cmul(v, gen_tw<1>(a.tw, t, M)));  // E_0 + W_M^t E_1
                     A(i) = fmaf(im(v), im(v), fmaf(re(v), re(v), A(i)));  // acquisition.py:149
                 }
+            }
             }
             __syncthreads();
         }
