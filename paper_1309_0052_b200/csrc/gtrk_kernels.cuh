@@ -6,7 +6,7 @@
 // chains: one CTA serves kEplChans = 32 channels, and
 //   - six consumer warps run the chains: warp j = 2 corr + comp, lane = channel, so every
 //     chain is one lane and a warp advances 32 of them per instruction;
-//   - kEplProducers producer warps stream the block through shared memory in chunks of
+//   - kEplProducers (16) producer warps stream the block through shared memory in chunks of
 //     kEplChunk samples (double-buffered, named barriers), writing for every (channel,
 //     sample) the six signed terms +-re / +-im of the wiped sample. The wipe is bit-exact:
 //     exact fixed-point NCOs (48-bit carrier mask, 42-bit code modulus 1023 * 2^42) evaluated
@@ -28,7 +28,10 @@ constexpr uint64_t kCarrierMask = (1ull << 48) - 1;
 constexpr uint64_t kCodeMod = 1023ull << 42;
 constexpr int kEplChans = 32;                       // channels per CTA: one per chain lane
 constexpr int kEplChunk = 64;                       // samples per chunk
-constexpr int kEplProducers = 8;                    // producer warps
+#ifndef GACQ_EPL_PRODUCERS
+#define GACQ_EPL_PRODUCERS 16
+#endif
+constexpr int kEplProducers = GACQ_EPL_PRODUCERS;   // producer warps (a divisor of 32)
 constexpr int kEplThreads = 32 * (6 + kEplProducers);
 constexpr int kEplRow = kEplChans + 1;              // padded: producers write along k, lanes = samples
 constexpr int kEplSmem = 2 * 6 * kEplChunk * kEplRow * (int)sizeof(float);  // 101,376 B
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(kEplThreads, 2) gacq_epl_kernel(const cx* __re
         if (lane < nc) out[(c0 + lane) * 6 + warp] = acc;
         return;
     }
-    // producers: warp pw owns channels pw, pw + 8, pw + 16, pw + 24; lane = sample in a half chunk
+    // producers: warp pw owns channels pw + kEplProducers j; lane = sample in a half chunk
     const int pw = warp - 6;
     const double inv = 6.283185307179586 / 281474976710656.0;  // TWO_PI / 2^48 (kernels.py:110)
     for (int c = 0; c < n_chunks; ++c) {
