@@ -103,8 +103,40 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
     const int64_t pair = a.pair0 + lp;
     const int64_t s = pair / a.B;
     const int b = (int)(pair % a.B);
-    wipe_fold<D, 32 * W>(reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh,
-                         reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh, a.P, a.K, wt);
+    const cx* xs = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh;
+    const cx* cs = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
+    // D = 4, K = 1 (C1-C3): chip sums computed in the wipe (wipe_chips4), wt then holds z[rho][m]
+    wipe_fold<D, 32 * W>(xs, cs, a.P, a.K, wt);
+    // D = W = 4 (C1-C3): the chip sums once per chip, in place. Thread t takes chips m = 128 j + t,
+    // reads wt[k][m] and wt[k][m + 1] (row 1023 repeats chip 0), and after a barrier overwrites
+    // wt[rho][m] = z_rho[m], summed in chip_sum's order (identical values); each warp then
+    // reads its z row instead of summing D entries per element.
+    constexpr bool zsum = D == 4 && W == 4;
+    if constexpr (zsum) {
+        constexpr int kIt = (kChips + 32 * W - 1) / (32 * W);
+        cx z[kIt][4];
+#pragma unroll
+        for (int j = 0; j < kIt; ++j) {
+            const int m = j * 32 * W + threadIdx.x;
+            if (m < kChips) {
+                cx v[7];
+#pragma unroll
+                for (int k = 0; k < 7; ++k) v[k] = k < 4 ? wt[k * WS + m] : wt[(k - 4) * WS + m + 1];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) z[j][r] = add2(add2(add2(add2(czero(), v[r]), v[r + 1]), v[r + 2]), v[r + 3]);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kIt; ++j) {
+            const int m = j * 32 * W + threadIdx.x;
+            if (m < kChips) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) wt[r * WS + m] = z[j][r];
+            }
+        }
+        __syncthreads();
+    }
 
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr bool kAlias = fwd_pfa_alias(D, W);
@@ -133,9 +165,9 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
             for (int n1 = 0; n1 < 31; ++n1) {
                 int m = mb + 33 * n1;
                 m -= m >= kChips ? kChips : 0;
-                zr[n1] = chip_sum(rho, m);
+                zr[n1] = zsum ? wt[rho * WS + m] : chip_sum(rho, m);
             }
-            ze = lane < 31 ? chip_sum(rho, me) : czero();
+            ze = lane < 31 ? (zsum ? wt[rho * WS + me] : chip_sum(rho, me)) : czero();
             if (kAlias) __syncthreads();  // every warp's chip sums are read before T overwrites wt
         } else {  // window [rho-1, rho-1+D) -> [rho, rho+D): drop wbar[D m + rho-1], add wbar[D (m+1) + rho-1]
             const cx* r = wt + (rho - 1) * WS;
