@@ -107,23 +107,29 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
     const cx* cs = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
     // D = 4, K = 1 (C1-C3): chip sums computed in the wipe (wipe_chips4), wt then holds z[rho][m]
     wipe_fold<D, 32 * W>(xs, cs, a.P, a.K, wt);
-    // D = W = 4 (C1-C3): the chip sums once per chip, in place. Thread t takes chips m = 128 j + t,
-    // reads wt[k][m] and wt[k][m + 1] (row 1023 repeats chip 0), and after a barrier overwrites
-    // wt[rho][m] = z_rho[m], summed in chip_sum's order (identical values); each warp then
-    // reads its z row instead of summing D entries per element.
-    constexpr bool zsum = D == 4 && W == 4;
+    // One phase per warp (W = D >= 4: C1-C3 at D = 4, the 8.184 MHz default at D = 8): the chip
+    // sums once per chip, in place. Thread t takes chips m = 32 W j + t, reads wt[k][m] and
+    // wt[k][m + 1] (row 1023 repeats chip 0), and after a barrier overwrites wt[rho][m] =
+    // z_rho[m], summed in chip_sum's order (identical values); each warp then reads its z row
+    // instead of summing D entries per element.
+    constexpr bool zsum = W == D && D >= 4;
     if constexpr (zsum) {
         constexpr int kIt = (kChips + 32 * W - 1) / (32 * W);
-        cx z[kIt][4];
+        cx z[kIt][D];
 #pragma unroll
         for (int j = 0; j < kIt; ++j) {
             const int m = j * 32 * W + threadIdx.x;
             if (m < kChips) {
-                cx v[7];
+                cx v[2 * D - 1];
 #pragma unroll
-                for (int k = 0; k < 7; ++k) v[k] = k < 4 ? wt[k * WS + m] : wt[(k - 4) * WS + m + 1];
+                for (int k = 0; k < 2 * D - 1; ++k) v[k] = k < D ? wt[k * WS + m] : wt[(k - D) * WS + m + 1];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) z[j][r] = add2(add2(add2(add2(czero(), v[r]), v[r + 1]), v[r + 2]), v[r + 3]);
+                for (int r = 0; r < D; ++r) {
+                    cx acc = czero();
+#pragma unroll
+                    for (int i = 0; i < D; ++i) acc = add2(acc, v[r + i]);
+                    z[j][r] = acc;
+                }
             }
         }
         __syncthreads();
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
             const int m = j * 32 * W + threadIdx.x;
             if (m < kChips) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) wt[r * WS + m] = z[j][r];
+                for (int r = 0; r < D; ++r) wt[r * WS + m] = z[j][r];
             }
         }
         __syncthreads();
