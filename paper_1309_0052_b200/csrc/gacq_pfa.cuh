@@ -143,6 +143,45 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
         }
         __syncthreads();
     }
+    // Several phases per warp (W < D: D = 13, 14, 16): all D chip sums per chip, in place,
+    // z_0 in full and z_rho by the one-sample slide the warps used for their later phases.
+    // Chips go in two batches of contiguous ranges, [0, 32 W kB) then the rest: a batch reads
+    // columns m and m + 1 of its own range (the first batch's last chip reads the second's first
+    // column, before the second writes), and column 1023 (the copy of chip 0) is never written.
+    constexpr bool zslide = W < D;
+    if constexpr (zslide) {
+        constexpr int kIt = (kChips + 32 * W - 1) / (32 * W);
+        constexpr int kB = (kIt + 1) / 2;
+#pragma unroll 1
+        for (int j0 = 0; j0 < kIt; j0 += kB) {
+            cx z[kB][D];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int m = (j0 + u) * 32 * W + threadIdx.x;
+                if (j0 + u < kIt && m < kChips) {
+                    cx acc = czero();
+#pragma unroll
+                    for (int i = 0; i < D; ++i) acc = add2(acc, wt[i * WS + m]);
+                    z[u][0] = acc;
+#pragma unroll
+                    for (int r = 1; r < D; ++r) {
+                        acc = add2(sub2(acc, wt[(r - 1) * WS + m]), wt[(r - 1) * WS + m + 1]);
+                        z[u][r] = acc;
+                    }
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int m = (j0 + u) * 32 * W + threadIdx.x;
+                if (j0 + u < kIt && m < kChips) {
+#pragma unroll
+                    for (int r = 0; r < D; ++r) wt[r * WS + m] = z[u][r];
+                }
+            }
+            __syncthreads();
+        }
+    }
 
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr bool kAlias = fwd_pfa_alias(D, W);
@@ -166,14 +205,23 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
     for (int ph = 0; ph < PWF; ++ph) {
         const int rho = rho0 + ph;
         if (rho >= D) break;
-        if (ph == 0) {
+        if (zsum || zslide) {  // the chip sums are in wt
 #pragma unroll
             for (int n1 = 0; n1 < 31; ++n1) {
                 int m = mb + 33 * n1;
                 m -= m >= kChips ? kChips : 0;
-                zr[n1] = zsum ? wt[rho * WS + m] : chip_sum(rho, m);
+                zr[n1] = wt[rho * WS + m];
             }
-            ze = lane < 31 ? (zsum ? wt[rho * WS + me] : chip_sum(rho, me)) : czero();
+            ze = lane < 31 ? wt[rho * WS + me] : czero();
+            if (kAlias && ph == 0) __syncthreads();  // every warp's chip sums are read before T overwrites wt
+        } else if (ph == 0) {
+#pragma unroll
+            for (int n1 = 0; n1 < 31; ++n1) {
+                int m = mb + 33 * n1;
+                m -= m >= kChips ? kChips : 0;
+                zr[n1] = chip_sum(rho, m);
+            }
+            ze = lane < 31 ? chip_sum(rho, me) : czero();
             if (kAlias) __syncthreads();  // every warp's chip sums are read before T overwrites wt
         } else {  // window [rho-1, rho-1+D) -> [rho, rho+D): drop wbar[D m + rho-1], add wbar[D (m+1) + rho-1]
             const cx* r = wt + (rho - 1) * WS;
