@@ -123,9 +123,10 @@ __device__ __forceinline__ void gen_dft(cx (&v)[R]) {
 // x[16 j' + r] would otherwise put a warp's 32 stores into one bank group)
 __device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
 
-template <int S, int R, int VPT>
+// kLoad: the first pass (logNs = 0, no twiddles) takes its inputs from load(i) instead of x[i]
+template <int S, int R, int VPT, bool kLoad = false, class Load = int>
 __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs, int logNs,
-                                                  const float2* __restrict__ tw, int L) {
+                                                  const float2* __restrict__ tw, int L, Load&& load = 0) {
     constexpr int kGroups = VPT / R;  // VPT values per thread (Ms <= VPT * blockDim)
     constexpr int kLogR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const int Ms = 1 << logMs, ng = Ms >> kLogR, Ns = 1 << logNs;
@@ -136,7 +137,12 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs,
         const int j = threadIdx.x + g * blockDim.x;
         if (j < ng) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) v[g][r] = x[gpad(j + r * ng)];
+            for (int r = 0; r < R; ++r) {
+                if constexpr (kLoad)
+                    v[g][r] = load(j + r * ng);
+                else
+                    v[g][r] = x[gpad(j + r * ng)];
+            }
             const int k = j & (Ns - 1);
             if (logNs > 0) {
                 // W^r from the table powers W^1, W^2, W^4, W^8 and at most two products each
@@ -181,6 +187,19 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs,
 template <int S, int VPT>
 __device__ __forceinline__ void gen_fft_stockham(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, int L) {
     int logNs = 0;
+    for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16, VPT>(x, logMs, logNs, tw, L);
+    const int rem = logMs - logNs;
+    if (rem == 3) gen_stockham_pass<S, 8, VPT>(x, logMs, logNs, tw, L);
+    else if (rem == 2) gen_stockham_pass<S, 4, VPT>(x, logMs, logNs, tw, L);
+    else if (rem == 1) gen_stockham_pass<S, 2, VPT>(x, logMs, logNs, tw, L);
+}
+// As gen_fft_stockham, with the first (radix-16, twiddle-free) pass reading load(i) for x[i]:
+// the inputs come straight from global memory, saving one shared-memory round trip and a barrier.
+template <int S, int VPT, class Load>
+__device__ __forceinline__ void gen_fft_stockham_ld(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, int L,
+                                                    Load&& load) {
+    gen_stockham_pass<S, 16, VPT, true>(x, logMs, 0, tw, L, load);
+    int logNs = 4;
     for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16, VPT>(x, logMs, logNs, tw, L);
     const int rem = logMs - logNs;
     if (rem == 3) gen_stockham_pass<S, 8, VPT>(x, logMs, logNs, tw, L);
@@ -270,13 +289,16 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M;
 #pragma unroll
         for (int part = 0; part < L; ++part) {
+#if GACQ_GEN_STOCKHAM
+            // Z . Cg read straight into the first pass (logMs >= 4 on this path)
+            gen_fft_stockham_ld<1, VPT>(sm, logMs, a.tw, L, [&](int k) {
+                return cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
+            });
+#else
 #pragma unroll 8  // keep 16 L2 loads in flight per thread
             for (int k = threadIdx.x; k < Ms; k += blockDim.x)
-                sm[GACQ_GEN_STOCKHAM ? gpad(k) : bitrev(k, logMs)] = cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
+                sm[bitrev(k, logMs)] = cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
             __syncthreads();
-#if GACQ_GEN_STOCKHAM
-            gen_fft_stockham<1, VPT>(sm, logMs, a.tw, L);
-#else
             gen_fft_inplace<1>(sm, logMs, a.tw, L);
 #endif
             if constexpr (kSmemAcc) {
