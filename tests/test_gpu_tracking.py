@@ -191,3 +191,23 @@ def test_track_step_degenerate_channel_in_a_later_slice(trk):
     with pytest.raises(trk.DegenerateInputError, match="all correlators zero on channel 4099"):
         trk.track_step(dev, offs, batch, cfg)
     np.testing.assert_array_equal(batch.code_phase_chips, before)
+
+
+def test_track_step_host_samples_equal_device_samples(trk):
+    """gacq_trk_step from a host buffer (staged H2D) and from a device buffer give identical epochs."""
+    import torch
+
+    c = case("chain_c3_snap0")
+    bl = blocks(c)
+    cfg = trk.TrackConfig(**c["config"])
+    n = bl[0].size
+    host = np.concatenate(bl[:3])
+    dev = torch.from_numpy(host).cuda()
+    b_h = b_d = trk.TrackBatch.from_states([to_state(trk, ch["init"]) for ch in c["channels"]])
+    for k in range(3):
+        offs = [k * n] * b_h.prn.size
+        b_h, o_h = trk.track_step(host, offs, b_h, cfg)
+        b_d, o_d = trk.track_step(dev, offs, b_d, cfg)
+        for key in o_h:
+            np.testing.assert_array_equal(o_h[key], o_d[key], err_msg=f"{k} {key}")
+    np.testing.assert_array_equal(b_h.carrier_phase_cycles, b_d.carrier_phase_cycles)
