@@ -244,19 +244,20 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
         const int n = j < N ? j : j - N;
         return cmul_exact(__ldg(&x[n]), __ldg(&c[n]));  // acquisition.py:141, kernels.py:78-86
     };
-#pragma unroll 4
-    for (int j = threadIdx.x; j < Ms; j += blockDim.x) {
+    auto input = [&](int j) {  // transform input j (the L = 2 split folds in its radix-2 step)
         cx y = wext(j);
         if (L == 2) {
             const cx u = wext(j + Ms);
             y = part == 0 ? add2(y, u) : cmul(sub2(y, u), gen_tw<-1>(a.tw, j, M));
         }
-        sm[GACQ_GEN_STOCKHAM ? gpad(j) : bitrev(j, logMs)] = y;
-    }
-    __syncthreads();
+        return y;
+    };
 #if GACQ_GEN_STOCKHAM
-    gen_fft_stockham<-1, VPT>(sm, logMs, a.tw, L);
+    gen_fft_stockham_ld<-1, VPT>(sm, logMs, a.tw, L, input);  // read straight into the first pass
 #else
+#pragma unroll 4
+    for (int j = threadIdx.x; j < Ms; j += blockDim.x) sm[bitrev(j, logMs)] = input(j);
+    __syncthreads();
     gen_fft_inplace<-1>(sm, logMs, a.tw, L);
 #endif
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
