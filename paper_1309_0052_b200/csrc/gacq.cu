@@ -365,13 +365,13 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
     int64_t waited = -1;
     std::vector<std::pair<size_t, int>> timed;  // (event index, kernel kind)
     // staged input: a short first chunk (its snapshots arrive first) hides the pipeline fill, and
-    // the chunks then double up to z_pairs, so each one waits only for the snapshots it reads
+    // the chunks then grow 4x up to z_pairs, so each one waits only for the snapshots it reads
     // while the copy stream stays ahead (H2D of a snapshot is ~10x faster than its search)
     int64_t want = !on_device ? std::min(c->z_pairs, std::max<int64_t>(copy_chunk * c->B, 2 * c->corr_slots / std::max(1, c->n_prn) + 1))
                               : c->z_pairs;
     for (int64_t p0 = 0, np = 0; p0 < n_pairs; p0 += np) {
         np = std::min(want, n_pairs - p0);
-        want = std::min(c->z_pairs, 2 * want);
+        want = std::min(c->z_pairs, 4 * want);
         if (!on_device) {
             const int64_t last_snap = (p0 + np - 1) / c->B;
             const int64_t need = last_snap / copy_chunk;
