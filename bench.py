@@ -62,8 +62,7 @@ CONFIGS = {
 
 
 # dominant (K2) kernel of each device path, gacq_info.path
-KERNEL_NAMES = {1: "gacq_corr_kernel (2048-point chip-polyphase)", 2: "gacq_corr_pfa_kernel (1023-point prime-factor)",
-                3: "gacq_corr_tc_kernel (1023-point prime-factor, 31-point stage on tcgen05)",
+KERNEL_NAMES = {2: "gacq_corr_pfa_kernel (1023-point prime-factor)",
                 4: "gacq_gen_corr_kernel (generic power-of-two path)"}
 
 

@@ -30,13 +30,17 @@
 extern "C" {
 #endif
 
-#define GACQ_ABI_VERSION 1
+#define GACQ_ABI_VERSION 2
 
 #define GACQ_OK 0
 #define GACQ_ERR_INVALID (-1)     /* -> InvalidInputError (errors.py:8-9)            */
 #define GACQ_ERR_UNSUPPORTED (-2) /* configuration outside the GPU path's support     */
 #define GACQ_ERR_CUDA (-3)        /* device / driver failure -> ResourceError          */
 #define GACQ_ERR_RESOURCE (-4)    /* allocation failure     -> ResourceError (24-25)   */
+
+/* gacq_params.plan_flags */
+#define GACQ_PLAN_GENERIC 1u    /* take the generic power-of-two path even at a chip-aligned
+                                   rate (parity tests of that path)                   */
 
 /* gacq_run flags */
 #define GACQ_SNAPS_ON_DEVICE 1u /* `snaps` is a device pointer (HBM-resident batch)   */
@@ -56,7 +60,7 @@ typedef struct gacq_params {
     int32_t n_prn;                    /* channels searched per snapshot, 1..32            */
     const int32_t* prns;              /* PRN numbers 1..32, distinct                      */
     int32_t device;                   /* CUDA ordinal                                     */
-    int32_t reserved;
+    int32_t plan_flags;               /* GACQ_PLAN_* (0 = default)                        */
     int64_t scratch_bytes;            /* spectrum scratch budget, 0 = default (1 GiB)     */
 } gacq_params;
 
@@ -74,13 +78,12 @@ typedef struct gacq_info {
     int32_t samples_per_period; /* P  = round(fs*1023/1.023e6) (acquisition.py:108-109) */
     int32_t n_coh;              /* samples per coherent block  (acquisition.py:116)     */
     int32_t chip_oversample;    /* D  = P / 1023 samples per chip                       */
-    int32_t fft_len;            /* transform length on the device: 1023 (path 2) or 2048 */
+    int32_t fft_len;            /* transform length on the device: 1023 (path 2) or M (path 4) */
     int32_t n_bins;
     int32_t n_prn;
     int32_t rounds;
-    int32_t path;               /* 2 = 1023-point prime-factor path (default),
-                                   1 = chip-polyphase 2048-point path (GACQ_PATH=2048),
-                                   3 = path 2 with the 31-point stage on the tensor cores */
+    int32_t path;               /* 2 = 1023-point prime-factor path (chip-aligned rates),
+                                   4 = generic power-of-two path (any other rate)         */
     int32_t corr_ctas;          /* persistent K2 grid (resident CTAs on the device)      */
 } gacq_info;
 
@@ -110,11 +113,19 @@ int gacq_create(gacq_ctx** out, const gacq_params* params);
 int gacq_info_get(const gacq_ctx* ctx, gacq_info* out);
 void gacq_destroy(gacq_ctx* ctx);
 
+/* Order the context's next device work after everything queued so far on `stream` (a
+ * cudaStream_t of the same device; (void*)1 = the legacy default stream, (void*)2 = the
+ * per-thread default stream): the __cuda_array_interface__ v3 "stream" contract for device
+ * inputs written by another library. */
+int gacq_wait_stream(gacq_ctx* ctx, void* stream);
+
 /* Search n_snap snapshots. Snapshot i starts at complex sample i*stride_samples of
  * `snaps` (interleaved float32 I/Q, complex64) and must hold >= rounds*n_coh samples;
  * only the first rounds*n_coh are read (acquisition.py:134-137). `rows` receives
  * n_snap*n_prn records (or n_snap*n_prn*n_bins with GACQ_ROWS_PER_BIN), ordered like the
- * plan's PRN list. Blocks until results are in `rows`. */
+ * plan's PRN list. Blocks until results are in `rows`. A snapshot holding a NaN or an
+ * infinity fails the call with GACQ_ERR_INVALID (the reference's IqBuffer refuses them,
+ * buffers.py:62-63); the rows of the other snapshots are still written. */
 int gacq_run(gacq_ctx* ctx, const void* snaps, int64_t n_snap, int64_t stride_samples,
              uint32_t flags, gacq_row* rows);
 
@@ -170,8 +181,8 @@ int gacq_stats_reset(gacq_ctx* ctx);
  * complex64 product) and the three E/P/L dot products against floor-indexed code replicas
  * of the 42-bit code NCO (kernels.py:116-128). The fixed-point starts and steps are given
  * per channel exactly as the reference computes them (kernels.py:56-70), so the replicas
- * are bit-identical; the dot products accumulate in float64 and round to float32 once
- * (the reference accumulates left to right in complex64: results agree to ~1e-6). */
+ * are bit-identical; the dot products are complex64 running sums taken left to right,
+ * exactly as the reference accumulates them (kernels.py:93-95): the sums are bit-identical. */
 typedef struct gacq_epl_chan {
     int64_t block_offset;  /* complex samples from `blocks` to this channel's first sample */
     uint64_t carrier_p0;   /* carrier_phase_to_fixed(state.carrier_phase_cycles)           */
@@ -185,6 +196,8 @@ typedef struct gacq_epl_chan {
 typedef struct gacq_trk gacq_trk;
 int gacq_trk_create(gacq_trk** out, int32_t device);
 void gacq_trk_destroy(gacq_trk* trk);
+/* gacq_wait_stream for the tracker's device work. */
+int gacq_trk_wait_stream(gacq_trk* trk, void* stream);
 /* out[c*6 + 0..5] = (ie, qe, ip, qp, il, ql) of channel c over n_samples samples.
  * `blocks` holds total_samples complex64 samples (host, or device with
  * GACQ_SNAPS_ON_DEVICE); every channel's block must lie inside it. */
@@ -232,7 +245,8 @@ int gacq_trk_chans(const gacq_trk_batch* batch, const gacq_trk_config* cfg, cons
 /* One tracking epoch of a whole batch in one call: gacq_trk_chans + gacq_trk_epl + gacq_trk_close
  * (tracking.py:126-275 for every channel), pipelined over channel slices so that one slice's
  * correlator kernel runs while the host computes the next slices' NCO words and closes the
- * previous ones. The block length is round(sample_rate_hz[0] * integration_ms / 1000). Results
+ * previous ones. The block length is round(sample_rate_hz[i] * integration_ms / 1000), which
+ * must be the same for every channel (GACQ_ERR_INVALID otherwise). Results
  * are those of the three calls: sums[c*6 + 0..5] the correlators, out[c*3 + 0..2] as
  * gacq_trk_close, the batch advanced in place. On a degenerate channel (*bad_channel = its
  * index, GACQ_ERR_INVALID) the batch may already be partly advanced: pass a copy (the Python

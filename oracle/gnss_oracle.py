@@ -18,6 +18,13 @@ Every floating-point operation is performed in the same order and precision as
 the reference (complex64 pipeline, float32 power map, float64 metric), so the
 outputs are bit-identical to the reference on this image; the golden fixtures
 under ``tests/golden`` pin that. Nothing here is imported by the product.
+
+Speed: like the reference (kernels.py:134-196, NUMBA_ENABLED), the per-sample
+loops -- complex product, |.|^2, carrier NCO -- run as numba-jitted twins when
+numba is importable (it is in this image and on the GPU box), so the CPU
+baseline times the reference's own execution model, not a slower numpy port.
+Both twins give identical bits (explicit float32 component arithmetic, no
+contraction); the golden tests run whichever is active.
 """
 
 from __future__ import annotations
@@ -27,6 +34,11 @@ from dataclasses import dataclass, field
 
 import numpy as np
 from scipy import fft as _sfft
+
+try:  # the reference's numba twins (kernels.py:134-196); numpy fallbacks below
+    from numba import njit as _njit
+except ImportError:  # pragma: no cover - numba is in the image
+    _njit = None
 
 CODE_LENGTH = 1023  # cacode.py:18
 CHIP_RATE_HZ = 1.023e6  # cacode.py:19
@@ -95,10 +107,14 @@ def code_step_to_fixed(chip_rate_hz: float, fs: float) -> int:
 
 def carrier_replica(phase_cycles: float, freq_hz: float, fs: float, n: int) -> np.ndarray:
     """exp(-2 pi i (p0 + k*step)/2^48) as complex64 -- gnss_signal.py:49-72 +
-    numpy twin kernels.py:106-114 (float64 cos/sin of the exact phase, then
+    kernels.py:106-114 / 175-185 (float64 cos/sin of the exact phase, then
     rounded to complex64 on assignment)."""
     p0 = carrier_phase_to_fixed(phase_cycles)
     step = carrier_step_to_fixed(freq_hz, fs)
+    if _njit is not None:
+        out = np.empty(n, dtype=np.complex64)
+        _carrier_nb(p0, step, n, out)
+        return out
     k = np.arange(n, dtype=np.uint64)
     phases = (np.uint64(p0) + k * np.uint64(step)) & np.uint64(CARRIER_SCALE - 1)
     theta = phases.astype(np.float64) * (_TWO_PI / CARRIER_SCALE)
@@ -131,7 +147,7 @@ def code_replica(chips: np.ndarray, phase_chips: float, fs: float, n: int) -> np
     return chips[idx].astype(np.complex64)
 
 
-def _cmul(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+def _cmul_np(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Naive complex64 product, real planes only -- kernels.py:78-86."""
     out = np.empty_like(a)
     out.real = a.real * b.real - a.imag * b.imag
@@ -139,9 +155,44 @@ def _cmul(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return out
 
 
-def _mag2(a: np.ndarray) -> np.ndarray:
+def _mag2_np(a: np.ndarray) -> np.ndarray:
     """kernels.py:89-90."""
     return a.real * a.real + a.imag * a.imag
+
+
+if _njit is not None:
+    @_njit(cache=True, nogil=True)
+    def _cmul_nb(a, b):
+        """kernels.py:137-145: the same float32 component formula, one sample at a time."""
+        out = np.empty_like(a)
+        for i in range(a.shape[0]):
+            ar, ai, br, bi = a[i].real, a[i].imag, b[i].real, b[i].imag
+            out[i] = complex(ar * br - ai * bi, ar * bi + ai * br)
+        return out
+
+    @_njit(cache=True, nogil=True)
+    def _mag2_nb(a):
+        """kernels.py:147-152."""
+        out = np.empty(a.shape[0], dtype=np.float32)
+        for i in range(a.shape[0]):
+            out[i] = a[i].real * a[i].real + a[i].imag * a[i].imag
+        return out
+
+    @_njit(cache=True, nogil=True)
+    def _carrier_nb(phase_fixed, step_fixed, n, out):
+        """kernels.py:175-185: 48-bit phase accumulator, float64 cos/sin."""
+        mask = np.uint64(CARRIER_SCALE - 1)
+        p = np.uint64(phase_fixed)
+        s = np.uint64(step_fixed)
+        inv = _TWO_PI / CARRIER_SCALE
+        for i in range(n):
+            theta = np.float64(p) * inv
+            out[i] = complex(math.cos(theta), -math.sin(theta))
+            p = (p + s) & mask
+
+    _cmul, _mag2 = _cmul_nb, _mag2_nb
+else:  # pragma: no cover
+    _cmul, _mag2 = _cmul_np, _mag2_np
 
 
 # --- synthesis (gnss_signal.py:136-186, harness.py:371-373) ----------------

@@ -13,6 +13,8 @@ LIB_PATH = Path(os.environ.get("GACQ_LIB") or Path(__file__).resolve().parent / 
 
 OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_CUDA, ERR_RESOURCE = 0, -1, -2, -3, -4
 SNAPS_ON_DEVICE, ROWS_ON_DEVICE, ROWS_PER_BIN, PROFILE = 1, 2, 4, 8
+PLAN_GENERIC = 1
+ABI_VERSION = 2
 
 
 class Params(C.Structure):
@@ -20,7 +22,7 @@ class Params(C.Structure):
                 ("noncoherent_rounds", C.c_int32), ("n_bins", C.c_int32),
                 ("doppler_bins_hz", C.POINTER(C.c_double)),
                 ("exclusion_radius_samples", C.c_int32), ("n_prn", C.c_int32),
-                ("prns", C.POINTER(C.c_int32)), ("device", C.c_int32), ("reserved", C.c_int32),
+                ("prns", C.POINTER(C.c_int32)), ("device", C.c_int32), ("plan_flags", C.c_int32),
                 ("scratch_bytes", C.c_int64)]
 
 
@@ -67,7 +69,8 @@ ROW_DTYPE = [("bin", "<i4"), ("lag", "<i4"), ("peak", "<f4"), ("floor", "<f4")]
 EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "gacq_destroy",
            "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
            "gacq_host_alloc", "gacq_host_free", "gacq_ca_code", "gacq_trk_create", "gacq_trk_destroy",
-           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth", "gacq_trk_close", "gacq_trk_chans", "gacq_trk_step")
+           "gacq_trk_epl", "gacq_carrier_table", "gacq_synth", "gacq_trk_close", "gacq_trk_chans", "gacq_trk_step",
+           "gacq_wait_stream", "gacq_trk_wait_stream")
 FMT_INT8, FMT_INT16 = 0, 1
 
 
@@ -104,7 +107,9 @@ def _load() -> C.CDLL:
     lib.gacq_trk_destroy.restype = None
     lib.gacq_trk_epl.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64, C.c_uint32,
                                  C.c_void_p]
-    if lib.gacq_version() != 1:
+    lib.gacq_wait_stream.argtypes = [C.c_void_p, C.c_void_p]
+    lib.gacq_trk_wait_stream.argtypes = [C.c_void_p, C.c_void_p]
+    if lib.gacq_version() != ABI_VERSION:
         raise ImportError("libgacq ABI version mismatch")
     return lib
 
@@ -131,3 +136,25 @@ def check(rc: int) -> None:
     if rc == ERR_UNSUPPORTED:
         raise UnsupportedError(msg)
     raise ResourceError(msg or f"libgacq error {rc}")
+
+
+def cai_stream(cai: dict):
+    """The stream a __cuda_array_interface__ producer wrote on, per the CAI v3 contract: None
+    when the producer says no synchronisation is needed, else a cudaStream_t handle (1 = the
+    legacy default stream, 2 = per-thread default). Producers without a "stream" key (v2) are
+    treated as writing on the legacy default stream."""
+    if "stream" not in cai:
+        return 1
+    st = cai["stream"]
+    if st is None:
+        return None
+    st = int(st)
+    return 1 if st == 0 else st
+
+
+def wait_for_producer(fn, handle, cai: dict) -> None:
+    """Order the library's device work after the producer's (gacq_wait_stream /
+    gacq_trk_wait_stream) before it reads a device array."""
+    st = cai_stream(cai)
+    if st is not None:
+        check(fn(handle, C.c_void_p(st)))

@@ -147,38 +147,51 @@ def _host_array(x) -> np.ndarray:
     return arr
 
 
-class PinnedBuffer:
-    """Page-locked host memory (gacq_host_alloc) viewed as a numpy array."""
+class _PinnedAlloc:
+    """Owner of one page-locked allocation (gacq_host_alloc). Every array view of it keeps
+    this object alive through its ``base`` chain, so the memory is freed (cudaFreeHost) only
+    when the last view is gone."""
 
-    def __init__(self, shape, dtype=np.complex64):
-        self.shape, self.dtype = tuple(shape), np.dtype(dtype)
-        nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+    def __init__(self, nbytes: int):
         self._ptr = C.c_void_p()
         _lib.check(_lib.lib.gacq_host_alloc(max(nbytes, 1), C.byref(self._ptr)))
-        buf = (C.c_char * max(nbytes, 1)).from_address(self._ptr.value)
-        self.array = np.frombuffer(buf, dtype=self.dtype, count=int(np.prod(self.shape))).reshape(self.shape)
-
-    def close(self):
-        if self._ptr:
-            self.array = None
-            _lib.lib.gacq_host_free(self._ptr)
-            self._ptr = C.c_void_p()
+        self.__array_interface__ = {"shape": (max(nbytes, 1),), "typestr": "|u1", "version": 3,
+                                    "data": (self._ptr.value, False)}
 
     def __del__(self):
         try:
-            self.close()
+            if self._ptr:
+                _lib.lib.gacq_host_free(self._ptr)
+                self._ptr = C.c_void_p()
         except Exception:  # noqa: BLE001 - interpreter shutdown
             pass
+
+
+class PinnedBuffer:
+    """Page-locked host memory viewed as a numpy array. ``array`` (and any view of it) owns
+    the allocation: it stays valid after this object is dropped or closed."""
+
+    def __init__(self, shape, dtype=np.complex64):
+        self.shape, self.dtype = tuple(shape), np.dtype(dtype)
+        count = int(np.prod(self.shape))
+        raw = np.asarray(_PinnedAlloc(count * self.dtype.itemsize))
+        self.array = raw[:count * self.dtype.itemsize].view(self.dtype).reshape(self.shape)
+
+    def close(self):
+        """Drop this object's reference; the memory is freed with the last array view."""
+        self.array = None
 
 
 class AcqEngine:
     """A search plan bound to one CUDA device (reference: acquire_all's per-call state)."""
 
     def __init__(self, sample_rate_hz: float, prns, config: AcqConfig | None = None,
-                 device: int = 0, scratch_bytes: int = 0, bin_range: tuple | None = None):
+                 device: int = 0, scratch_bytes: int = 0, bin_range: tuple | None = None,
+                 force_generic: bool = False):
         """``bin_range=(b0, b1)`` searches only bins [b0, b1) of the config's grid (Doppler-bin
         sharding of one snapshot over devices); rows then carry grid-global
-        bin indices, so per-shard rows merge with ``merge_bin_shards``."""
+        bin indices, so per-shard rows merge with ``merge_bin_shards``. ``force_generic`` takes
+        the generic power-of-two path at a chip-aligned rate too (parity tests of that path)."""
         config = config or AcqConfig()
         prns = [int(p) for p in prns]
         if not prns:
@@ -210,7 +223,7 @@ class AcqEngine:
         params = _lib.Params(fs, config.coherent_ms, config.noncoherent_rounds, self._bins_c.size,
                              self._bins_c.ctypes.data_as(C.POINTER(C.c_double)), self.radius,
                              len(prns), self.prns.ctypes.data_as(C.POINTER(C.c_int32)), self.device,
-                             0, int(scratch_bytes))
+                             _lib.PLAN_GENERIC if force_generic else 0, int(scratch_bytes))
         self._ctx = C.c_void_p()
         _lib.check(_lib.lib.gacq_create(C.byref(self._ctx), C.byref(params)))
         info = _lib.Info()
@@ -237,6 +250,7 @@ class AcqEngine:
                 raise InvalidInputError("device snapshots must be contiguous along samples")
             ptr = cai["data"][0]
             flags |= _lib.SNAPS_ON_DEVICE
+            _lib.wait_for_producer(_lib.lib.gacq_wait_stream, self._ctx, cai)
         else:
             arr = _host_array(snapshots)
             n_snap, n_samp = arr.shape
@@ -283,6 +297,7 @@ class AcqEngine:
             row = strides[0] // want.itemsize if strides and len(strides) == 2 else shape[1]
             ptr = cai["data"][0]
             flags |= _lib.SNAPS_ON_DEVICE
+            _lib.wait_for_producer(_lib.lib.gacq_wait_stream, self._ctx, cai)
         else:
             arr = np.asarray(iq)
             if arr.dtype != want:

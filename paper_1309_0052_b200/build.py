@@ -16,7 +16,7 @@ ROOT = PKG.parent
 LIB = PKG / "libgacq.so"
 SOURCES = [PKG / "csrc" / "gacq.cu"]
 DEPS = SOURCES + [PKG / "csrc" / h for h in ("gacq_kernels.cuh", "gacq_pfa.cuh", "pfa.cuh", "pfa_tables.cuh",
-                                             "codelets.cuh", "gtrk_kernels.cuh", "gacq_tc.cuh", "tc_util.cuh", "gacq_tables.cuh", "gacq_generic.cuh", "rader31.cuh", "gtrk_close.h")] + [ROOT / "include" / "gacq.h"]
+                                             "codelets.cuh", "gtrk_kernels.cuh", "gacq_tables.cuh", "gacq_generic.cuh", "rader31.cuh", "gtrk_close.h")] + [ROOT / "include" / "gacq.h"]
 
 
 def nvcc() -> str:

@@ -24,7 +24,6 @@
 
 #include "gacq_kernels.cuh"
 #include "gacq_pfa.cuh"
-#include "gacq_tc.cuh"
 #include "gacq_tables.cuh"
 #include "gacq_generic.cuh"
 #include "gtrk_kernels.cuh"
@@ -108,13 +107,6 @@ void fft_f64(std::vector<std::complex<double>>& a) {
     }
 }
 
-// natural index n of a 2048-point spectrum -> float2 slot of the permuted layout that
-// lets thread t of a 128-thread transform fetch x[t + 128 r'] as 8 float4 loads
-inline int perm_slot(int n) {
-    const int rp = n >> 7, t = n & 127;
-    return (rp >> 1) * 256 + 2 * t + (rp & 1);
-}
-
 }  // namespace
 
 struct gacq_ctx {
@@ -122,12 +114,8 @@ struct gacq_ctx {
     int device = 0;
     double fs = 0;
     int n_coh = 0, P = 0, D = 0, K = 0, R = 0, B = 0, n_prn = 0, radius = 0;
-    int ng = 1;  // K1 transform groups per CTA (2048-point path)
-    bool pfa = true;  // 1023-point prime-factor path (gacq_pfa.cuh); GACQ_PATH=2048 selects the other
     int cw = 4, cpw = 1;  // PFA K2: warps per CTA, phases per warp
-    bool tc = false;      // PFA K2 with the 31-point stage on the tensor cores (gacq_tc.cuh)
-    float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kBuf]
-    float* d_tcB = nullptr;   // tensor-core 31-point inverse DFT matrix, hi and lo [2][64*64]
+    float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kCcHalf]
     bool gen = false;         // generic power-of-two path (rates that are not chip-aligned)
     int logM = 0;             // its transform length M = 2^logM >= n_coh + P - 1
     float2* d_gtw = nullptr;  // [M/2] (cos, sin)(2 pi e / M)
@@ -136,9 +124,7 @@ struct gacq_ctx {
     std::vector<int32_t> prns;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     float2* d_carrier = nullptr;
-    float4* d_cc = nullptr;
-    float2* d_tw = nullptr;
-    float4* d_Z = nullptr;
+    cx* d_Z = nullptr;
     int64_t z_pairs = 0;  // pairs per chunk that fit in the scratch
     float2* d_in = nullptr;
     int64_t in_cap = 0;   // complex64 staging (samples)
@@ -152,8 +138,11 @@ struct gacq_ctx {
     float* d_row_scratch = nullptr;  // [corr_slots][D*1024] power rows when D > 4
     int64_t corr_slots = 0;          // resident K2 CTAs (persistent grid)
     unsigned long long* d_counter = nullptr;  // K2 work counter
+    int* d_bad = nullptr;   // lowest snapshot index holding a non-finite sample (K1 atomicMin)
+    int* h_bad = nullptr;   // pinned copy of d_bad
     std::vector<cudaEvent_t> copy_events;
     std::vector<cudaEvent_t> prof_events;
+    cudaEvent_t wait_event = nullptr;  // gacq_wait_stream
     gacq_stats stats{};
 };
 
@@ -184,35 +173,16 @@ int grow(T** ptr, int64_t* cap, int64_t need) {
     return GACQ_OK;
 }
 
-int fwd_smem_bytes(const gacq_ctx* c) { return (int)sizeof(float2) * (c->D * fwd_ws(c->D) + c->ng * 2 * kXchg); }
-bool corr_row_in_smem(const gacq_ctx* c) { return c->D <= 4; }
-int corr_smem_bytes(const gacq_ctx* c) { return corr_row_in_smem(c) ? (int)sizeof(float) * c->D * kRow : 0; }
-
-// K1 instantiations: (transform groups per CTA, chip oversampling D) for every D <= 16 at
-// which the reference's 42-bit code NCO is exactly chip-aligned (checked in gacq_create)
-#define GACQ_FWD_VARIANTS(X) X(1, 1) X(2, 2) X(2, 4) X(2, 5) X(2, 6) X(2, 8) X(2, 13) X(2, 14) X(2, 16)
-
-cudaError_t launch_fwd(const gacq_ctx* c, const FwdArgs& fa, int64_t blocks) {
-    const int smem = fwd_smem_bytes(c);
-#define GACQ_LAUNCH_FWD(NG, DD)                                                       \
-    if (c->D == DD) {                                                                 \
-        gacq_fwd_kernel<NG, DD><<<(unsigned)blocks, NG * kT, smem, c->stream>>>(fa); \
-        return cudaGetLastError();                                                    \
-    }
-    GACQ_FWD_VARIANTS(GACQ_LAUNCH_FWD)
-#undef GACQ_LAUNCH_FWD
-    return cudaErrorInvalidConfiguration;
-}
+// PFA K1 instantiations: (D, warps per CTA) for every D <= 16 at which the reference's 42-bit
+// code NCO is exactly chip-aligned (checked in gacq_create)
+#define GACQ_PFA_FWD_VARIANTS(X) X(1, 1) X(2, 2) X(4, 4) X(5, 5) X(6, 6) X(8, 8) X(13, 7) X(14, 7) X(16, 8)
 
 bool fwd_supported(int D) {
-#define GACQ_HAS_FWD(NG, DD) if (D == DD) return true;
-    GACQ_FWD_VARIANTS(GACQ_HAS_FWD)
+#define GACQ_HAS_FWD(DD, WW) if (D == DD) return true;
+    GACQ_PFA_FWD_VARIANTS(GACQ_HAS_FWD)
 #undef GACQ_HAS_FWD
     return false;
 }
-
-// PFA K1 instantiations: (D, warps per CTA)
-#define GACQ_PFA_FWD_VARIANTS(X) X(1, 1) X(2, 2) X(4, 4) X(5, 5) X(6, 6) X(8, 8) X(13, 7) X(14, 7) X(16, 8)
 
 cudaError_t launch_fwd_pfa(const gacq_ctx* c, const FwdPfaArgs& fa, int64_t blocks) {
 #define GACQ_LAUNCH_FWDP(DD, WW)                                                                        \
@@ -239,27 +209,10 @@ void corr_pfa_shape(int D, int* W, int* PW) {
 cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
     if (ca.n_items + c->corr_slots >= INT32_MAX) return cudaErrorInvalidValue;  // 32-bit item indices
-    if (c->tc) {
-        const float4* B = reinterpret_cast<const float4*>(c->d_tcB);
-        if (c->cpw == 1)
-            gacq_corr_tc_kernel<true><<<(unsigned)blocks, 32 * kTcWarps, corr_tc_smem(), c->stream>>>(ca, B);
-        else
-            gacq_corr_tc_kernel<false><<<(unsigned)blocks, 32 * kTcWarps, corr_tc_smem(), c->stream>>>(ca, B);
-        return cudaGetLastError();
-    }
     if (c->cpw == 1)
         gacq_corr_pfa_kernel<true><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
     else
         gacq_corr_pfa_kernel<false><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_corr(const gacq_ctx* c, const CorrArgs& ca) {
-    const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
-    if (corr_row_in_smem(c))
-        gacq_corr_kernel<true><<<(unsigned)blocks, kT, corr_smem_bytes(c), c->stream>>>(ca);
-    else
-        gacq_corr_kernel<false><<<(unsigned)blocks, kT, corr_smem_bytes(c), c->stream>>>(ca);
     return cudaGetLastError();
 }
 
@@ -319,6 +272,8 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         run_end = prof_event(c, 1);
         CUDA_TRY(cudaEventRecord(run_start, staged ? c->copy_stream : c->stream));
     }
+    // K1 lowers d_bad to the index of any snapshot holding a NaN or an infinity
+    CUDA_TRY(cudaMemsetAsync(c->d_bad, 0x7f, sizeof(int), c->stream));
     const float2* in = (const float2*)inp.ptr;
     int64_t in_stride = inp.stride;
     // Staging in snapshot chunks on the copy stream (H2D and/or dequantization);
@@ -382,7 +337,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         cx* Zp = reinterpret_cast<cx*>(c->d_Z);
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
         GenArgs ga{in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
-                   pmap, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
+                   pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
         const int gen_l = c->logM > kGenMaxLogM ? 2 : 1;
         const int gen_pts = (1 << c->logM) / gen_l;
         const int gen_smem = (int)sizeof(float2) * (GACQ_GEN_STOCKHAM ? gen_pts + gen_pts / 16 : gen_pts);
@@ -395,12 +350,9 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             else
                 gacq_gen_fwd_kernel<1, 32><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
-        } else if (c->pfa) {
-            FwdPfaArgs fa{in, in_stride, c->d_carrier, Zp, p0, c->B, c->R, c->n_coh, c->P, c->K};
-            CUDA_TRY(launch_fwd_pfa(c, fa, np * c->R));
         } else {
-            FwdArgs fa{in, in_stride, c->d_carrier, c->d_tw, c->d_Z, p0, c->B, c->R, c->n_coh, c->P, c->D, c->K};
-            CUDA_TRY(launch_fwd(c, fa, np * c->R));
+            FwdPfaArgs fa{in, in_stride, c->d_carrier, Zp, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->K};
+            CUDA_TRY(launch_fwd_pfa(c, fa, np * c->R));
         }
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
         if (!c->gen) CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
@@ -414,15 +366,11 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             else
                 gacq_gen_corr_kernel<1, 32><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
-        } else if (c->pfa) {
+        } else {
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
                            np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw, 0,
                            (unsigned)(((1ull << 32) + c->D - 1) / c->D)};
             CUDA_TRY(launch_corr_pfa(c, ca));
-        } else {
-            CorrArgs ca{c->d_Z, c->d_cc, c->d_tw, c->d_rows_bin, pmap, c->d_row_scratch, p0, np * c->n_prn,
-                        c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius};
-            CUDA_TRY(launch_corr(c, ca));
         }
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }
         c->stats.fwd_launches++;
@@ -451,6 +399,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             c->stats.d2h_bytes += n_out * (int64_t)sizeof(gacq_row);
         }
     }
+    CUDA_TRY(cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (profile) CUDA_TRY(cudaEventRecord(run_end, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (!on_device) CUDA_TRY(cudaStreamSynchronize(c->copy_stream));
@@ -466,6 +415,10 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
     }
     c->stats.calls++;
     c->stats.cells += n_snap * c->n_prn * c->B;
+    // the reference refuses such buffers (IqBuffer, buffers.py:62-63); rows of the other
+    // snapshots are valid
+    if (*c->h_bad < n_snap)
+        return fail(GACQ_ERR_INVALID, "IqBuffer samples must be finite (snapshot %d)", *c->h_bad);
     return GACQ_OK;
 }
 
@@ -475,11 +428,8 @@ void destroy_ctx(gacq_ctx* c) {
         DeviceGuard g(c->device);
         if (c->stream) cudaStreamSynchronize(c->stream);
         cudaFree(c->d_carrier);
-        cudaFree(c->d_cc);
-        cudaFree(c->d_tw);
         cudaFree(c->d_Z);
         cudaFree(c->d_ccp);
-        cudaFree(c->d_tcB);
         cudaFree(c->d_gtw);
         cudaFree(c->d_gcc);
         cudaFree(c->d_in);
@@ -489,8 +439,11 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_pmap);
         cudaFree(c->d_row_scratch);
         cudaFree(c->d_counter);
+        cudaFree(c->d_bad);
+        if (c->h_bad) cudaFreeHost(c->h_bad);
         for (auto e : c->copy_events) cudaEventDestroy(e);
         for (auto e : c->prof_events) cudaEventDestroy(e);
+        if (c->wait_event) cudaEventDestroy(c->wait_event);
         if (c->stream) cudaStreamDestroy(c->stream);
         if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     }
@@ -545,8 +498,7 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
             ph = (ph + code_step) % kCodeModulus;
         }
     }
-    const char* path_env = std::getenv("GACQ_PATH");
-    const bool gen = !aligned || (path_env && std::strcmp(path_env, "generic") == 0);
+    const bool gen = !aligned || (p->plan_flags & GACQ_PLAN_GENERIC);
     int logM = 0;
     if (gen) {
         // n_coh a power of two: the reference's n_coh-point circular correlation is the M = n_coh
@@ -581,21 +533,9 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->B = p->n_bins;
     c->n_prn = p->n_prn;
     c->radius = p->exclusion_radius_samples ? p->exclusion_radius_samples : (int)std::ceil(fs / kChipRate);
-    c->ng = D >= 2 ? 2 : 1;
-    if (const char* ev = std::getenv("GACQ_PATH")) c->pfa = std::strcmp(ev, "2048") != 0;
     c->gen = gen;
     c->logM = logM;
-    if (gen) c->pfa = false;
     if (!gen) corr_pfa_shape(D, &c->cw, &c->cpw);
-    {
-        const char* ev = std::getenv("GACQ_TC");
-        // opt-in (GACQ_TC=1): measured slower than the FP32 kernel on B200, see DESIGN.md section 5
-        c->tc = c->pfa && D % kTcWarps == 0 && ev && std::strcmp(ev, "1") == 0;
-        if (c->tc) {
-            c->cw = kTcWarps;
-            c->cpw = D / kTcWarps;
-        }
-    }
     c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
     c->prns.assign(p->prns, p->prns + p->n_prn);
 
@@ -607,50 +547,6 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     std::vector<uint64_t> steps(c->B);
     for (int b = 0; b < c->B; ++b)
         steps[b] = (uint64_t)py_mod(py_round((c->bins[b] / fs) * (double)kCarrierScale), kCarrierScale);
-    // 2048-point path (GACQ_PATH=2048) tables: conjugate code spectra / 2048 of
-    // d[j] = chip[j mod 1023], j < 2046, in the permuted layout, and twiddles
-    std::vector<float2> cc, tw;
-    if (!c->pfa && !gen) {
-        cc.resize((size_t)c->n_prn * kM);
-        for (int i = 0; i < c->n_prn; ++i) {
-            int8_t chips[1023];
-            ca_code(c->prns[i], chips);
-            std::vector<std::complex<double>> d(kM, 0.0);
-            for (int j = 0; j < 2 * 1023; ++j) d[j] = (double)chips[j % 1023];
-            fft_f64(d);
-            for (int k = 0; k < kM; ++k) {
-                const auto v = std::conj(d[k]) / (double)kM;
-                cc[(size_t)i * kM + perm_slot(k)] = make_float2((float)v.real(), (float)v.imag());
-            }
-        }
-        tw.resize(kM);
-        for (int e = 0; e < kM; ++e)
-            tw[e] = make_float2((float)std::cos(kTwoPi * e / kM), (float)std::sin(kTwoPi * e / kM));
-    }
-
-    // tensor-core 31-point inverse DFT (gacq_tc.cuh): B[2 k1 + c][2 q1 + c'] is the real form of
-    // exp(+2 pi i k1 q1 / 31), stored as [n = 2 q1 + c'][k = 2 k1 + c] in core-matrix order, split
-    // into hi (top 19 bits, what TF32 reads) and lo = B - hi
-    std::vector<float> tcB(2 * kTcB, 0.f);
-    for (int k1 = 0; k1 < 31; ++k1)
-        for (int q1 = 0; q1 < 31; ++q1) {
-            const double th = kTwoPi * (double)((k1 * q1) % 31) / 31.0;
-            const float cs = (float)std::cos(th), sn = (float)std::sin(th);
-            const float val[2][2] = {{cs, sn}, {-sn, cs}};  // [c][c']: re/im of the input x re/im of the output
-            for (int cc = 0; cc < 2; ++cc)
-                for (int co = 0; co < 2; ++co) {
-                    const float b = val[cc][co];
-                    uint32_t u;
-                    std::memcpy(&u, &b, 4);
-                    u &= 0xffffe000u;
-                    float hi;
-                    std::memcpy(&hi, &u, 4);
-                    const int off = tc_b_off(2 * q1 + co, 2 * k1 + cc);
-                    tcB[off] = hi;
-                    tcB[kTcB + off] = b - hi;
-                }
-        }
-
     // generic path: conj(DFT_M(c)) / M of each PRN's sampled code replica c[n], n < n_coh,
     // chip index (k * step mod 1023*2^42) >> 42 (kernels.py:116-128, acquisition.py:88-105),
     // in float64 then rounded once; twiddles (cos, sin)(2 pi e / M)
@@ -734,12 +630,6 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         cudaFree(d_chips);
         CTX_TRY(te);
     }
-    if (!c->pfa && !gen) {
-        CTX_TRY(cudaMalloc(&c->d_cc, cc.size() * sizeof(float2)));
-        CTX_TRY(cudaMalloc(&c->d_tw, tw.size() * sizeof(float2)));
-        CTX_TRY(cudaMemcpy(c->d_cc, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice));
-        CTX_TRY(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-    }
     if (gen) {
         CTX_TRY(cudaMalloc(&c->d_gcc, gcc.size() * sizeof(float2)));
         CTX_TRY(cudaMalloc(&c->d_gtw, gtw.size() * sizeof(float2)));
@@ -754,26 +644,18 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, corr1_max));
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
     }
-    const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * (c->pfa ? kBuf : kM)) *
+    const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * kBuf) *
                                (int64_t)sizeof(float2);
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
+    CTX_TRY(cudaMalloc(&c->d_bad, sizeof(int)));
+    CTX_TRY(cudaHostAlloc(&c->h_bad, sizeof(int), cudaHostAllocPortable));
     if (gen) {
         *out = c;
         return GACQ_OK;
     }
-    if (c->tc) {
-        CTX_TRY(cudaMalloc(&c->d_tcB, tcB.size() * sizeof(float)));
-        CTX_TRY(cudaMemcpy(c->d_tcB, tcB.data(), tcB.size() * sizeof(float), cudaMemcpyHostToDevice));
-        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     corr_tc_smem()));
-        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     corr_tc_smem()));
-        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        CTX_TRY(cudaFuncSetAttribute(gacq_corr_tc_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    }
-    if (c->pfa) {
+    {
         // every PFA variant gets the largest dynamic shared memory any plan launches it with
         CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      corr_pfa_smem(kCorrMaxWarps)));
@@ -785,51 +667,18 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         GACQ_PFA_FWD_VARIANTS(GACQ_ATTR_FWDP)
 #undef GACQ_ATTR_FWDP
         int per_sm = 0, sms = 0;
-        if (c->tc)
-            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, c->cpw == 1 ? gacq_corr_tc_kernel<true>
-                                                                                    : gacq_corr_tc_kernel<false>,
-                                                                  32 * kTcWarps, corr_tc_smem()));
-        else if (c->cpw == 1)
+        if (c->cpw == 1)
             CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<true>, 32 * c->cw,
                                                                   corr_pfa_smem(c->cw)));
         else
             CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<false>, 32 * c->cw,
                                                                   corr_pfa_smem(c->cw)));
         CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-        if (const char* ev = std::getenv("GACQ_CORR_CTAS_PER_SM")) per_sm = std::atoi(ev);
         c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
         if (c->cpw > 1)
             CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kChips * sizeof(float)));
         CTX_TRY(cudaMalloc(&c->d_counter, sizeof(unsigned long long)));
-        *out = c;
-        return GACQ_OK;
     }
-    // Function attributes are process-wide (shared by every plan), so each kernel gets the
-    // largest dynamic shared memory any plan can launch it with -- a function of its
-    // template parameters only, never of this plan.
-    const int csm = corr_smem_bytes(c);
-    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(float) * 4 * kRow));
-    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    CTX_TRY(cudaFuncSetAttribute(gacq_corr_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    {
-        int per_sm = 0, sms = 0;
-        if (corr_row_in_smem(c))
-            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_kernel<true>, kT, csm));
-        else
-            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_kernel<false>, kT, 0));
-        CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-        c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
-    }
-    if (!corr_row_in_smem(c))
-        CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kRow * sizeof(float)));
-    CTX_TRY(cudaMalloc(&c->d_counter, sizeof(unsigned long long)));
-#define GACQ_ATTR_FWD(NG, DM)                                                                 \
-    CTX_TRY(cudaFuncSetAttribute(gacq_fwd_kernel<NG, DM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)sizeof(float2) * (DM * fwd_ws(DM) + NG * 2 * kXchg)));
-    GACQ_FWD_VARIANTS(GACQ_ATTR_FWD)
-#undef GACQ_ATTR_FWD
-
 #undef CTX_TRY
     *out = c;
     return GACQ_OK;
@@ -840,16 +689,27 @@ int gacq_info_get(const gacq_ctx* c, gacq_info* o) {
     o->samples_per_period = c->P;
     o->n_coh = c->n_coh;
     o->chip_oversample = c->D;
-    o->fft_len = c->gen ? (1 << c->logM) : c->pfa ? kChips : kM;
+    o->fft_len = c->gen ? (1 << c->logM) : kChips;
     o->n_bins = c->B;
     o->n_prn = c->n_prn;
     o->rounds = c->R;
-    o->path = c->gen ? 4 : c->tc ? 3 : c->pfa ? 2 : 1;
+    o->path = c->gen ? 4 : 2;
     o->corr_ctas = (int32_t)c->corr_slots;
     return GACQ_OK;
 }
 
 void gacq_destroy(gacq_ctx* c) { destroy_ctx(c); }
+
+int gacq_wait_stream(gacq_ctx* c, void* stream) {
+    if (!c) return fail(GACQ_ERR_INVALID, "null context");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (!c->wait_event) CUDA_TRY(cudaEventCreateWithFlags(&c->wait_event, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(c->wait_event, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->wait_event, 0));
+    CUDA_TRY(cudaStreamWaitEvent(c->copy_stream, c->wait_event, 0));
+    return GACQ_OK;
+}
 
 int gacq_run(gacq_ctx* c, const void* snaps, int64_t n_snap, int64_t stride, uint32_t flags, gacq_row* rows) {
     if (!c) return fail(GACQ_ERR_INVALID, "null context");
@@ -950,7 +810,7 @@ int gacq_synth(int32_t device, double fs, int64_t n_snap, int64_t n, int32_t n_s
         cudaError_t e;
         std::vector<int32_t> all(32);
         for (int i = 0; i < 32; ++i) all[i] = i + 1;
-        if ((e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking)) ||
+        if ((e = cudaStreamCreateWithFlags(&stream, cudaStreamDefault)) ||  // ordered after the legacy default stream
             (e = cudaMalloc(&d_st, std::max<size_t>(1, st.size()) * sizeof(SynthSat))) ||
             (e = cudaMalloc(&d_prns, 32 * sizeof(int32_t))) || (e = cudaMalloc(&d_chips, 32 * kChips)))
             return e;
@@ -1019,6 +879,7 @@ struct gacq_trk {
     float* h_sums = nullptr;
     int64_t h_cap = 0;                 // channels
     std::vector<cudaEvent_t> slice_events;
+    cudaEvent_t wait_event = nullptr;  // gacq_trk_wait_stream
 };
 
 static void trk_free(gacq_trk* t) {
@@ -1033,6 +894,7 @@ static void trk_free(gacq_trk* t) {
         cudaFreeHost(t->h_chans);
         cudaFreeHost(t->h_sums);
         for (cudaEvent_t e : t->slice_events) cudaEventDestroy(e);
+        if (t->wait_event) cudaEventDestroy(t->wait_event);
         if (t->stream) cudaStreamDestroy(t->stream);
     }
     delete t;
@@ -1067,6 +929,16 @@ int gacq_trk_create(gacq_trk** out, int32_t device) {
 
 void gacq_trk_destroy(gacq_trk* t) { trk_free(t); }
 
+int gacq_trk_wait_stream(gacq_trk* t, void* stream) {
+    if (!t) return fail(GACQ_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    if (!t->wait_event) CUDA_TRY(cudaEventCreateWithFlags(&t->wait_event, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(t->wait_event, (cudaStream_t)stream));
+    CUDA_TRY(cudaStreamWaitEvent(t->stream, t->wait_event, 0));
+    return GACQ_OK;
+}
+
 }  // extern "C"
 
 namespace gtrk {
@@ -1075,11 +947,9 @@ namespace gtrk {
 struct Closure {
     const gacq_trk_config* cfg;
     double sp, t, g1p, g2p, g1d, g2d, alpha;
-    int64_t n;
-    Closure(const gacq_trk_batch* b, const gacq_trk_config* c) : cfg(c) {
+    explicit Closure(const gacq_trk_config* c) : cfg(c) {
         sp = c->correlator_spacing_chips;
         t = c->integration_ms * 1e-3;
-        n = rint64(b->sample_rate_hz[0] * c->integration_ms * 1e-3);  // tracking.py:122-123
         auto gains = [](double bw, double* g1, double* g2) {  // tracking.py:188-190
             const double w0 = bw / 0.53;
             *g1 = 2.0 * kLoopDamping * w0;
@@ -1112,6 +982,7 @@ struct Closure {
                 const double ed = e + l == 0 ? 0.0 : (e - l) / (e + l) * (1.0 - sp / 2.0) / 2.0;
                 const double ep = ip == 0.0 ? std::copysign(0.25, qp) : std::atan(qp / ip) / two_pi;  // :179-185
                 const double fs = b->sample_rate_hz[i];
+                const int64_t n = rint64(fs * cfg->integration_ms * 1e-3);  // the channel's block, tracking.py:122-123
                 const double pll_acc = b->pll_acc[i] + g2p * t * (ep + b->pll_prev[i]) / 2.0;  // :198-200
                 const double dll_acc = b->dll_acc[i] + g2d * t * (ed + b->dll_prev[i]) / 2.0;
                 const double doppler = b->doppler_hz[i] + (pll_acc - b->pll_acc[i]);  // :242
@@ -1182,7 +1053,7 @@ int gacq_trk_close(const float* sums, const gacq_trk_batch* b, const gacq_trk_co
         return fail(GACQ_ERR_INVALID, "%s on channel %lld", all ? "all correlators zero" : "prompt correlator is zero",
                     (long long)i);
     }
-    gtrk::Closure(b, cfg).range(sums, b, out, 0, b->n);
+    gtrk::Closure(cfg).range(sums, b, out, 0, b->n);
     return GACQ_OK;
 }
 
@@ -1239,6 +1110,11 @@ int gacq_trk_step(gacq_trk* t, const void* blocks, int64_t total, const int64_t*
     const int n = (int)n64;
     for (int64_t i = 0; i < nch; ++i) {
         if (b->prn[i] < 1 || b->prn[i] > 32) return fail(GACQ_ERR_INVALID, "prn must be an integer in 1..32, got %d", b->prn[i]);
+        // one correlator launch covers the batch: every channel's own block length
+        // (tracking.py:122-123) must be the launch's
+        if (gtrk::rint64(b->sample_rate_hz[i] * cfg->integration_ms * 1e-3) != n64)
+            return fail(GACQ_ERR_INVALID, "channel %lld: block length differs from channel 0's (mixed sample rates)",
+                        (long long)i);
         if (offsets[i] < 0 || offsets[i] + n > total)
             return fail(GACQ_ERR_INVALID, "channel %lld block outside the sample buffer", (long long)i);
     }
@@ -1293,7 +1169,7 @@ int gacq_trk_step(gacq_trk* t, const void* blocks, int64_t total, const int64_t*
             cudaEventRecord(t->slice_events[k], t->stream) != cudaSuccess)
             return drain(fail(GACQ_ERR_CUDA, "correlator launch failed"));
     }
-    gtrk::Closure cl(b, cfg);
+    gtrk::Closure cl(cfg);
     for (int64_t k = 0; k < n_slices; ++k) {
         const int64_t a = k * slice, e = std::min(nch, a + slice);
         if (cudaEventSynchronize(t->slice_events[k]) != cudaSuccess)

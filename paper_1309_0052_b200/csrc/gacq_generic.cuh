@@ -220,6 +220,7 @@ struct GenArgs {
     cx* Z;                  // [pairs_in_chunk][R][M] spectra, residue-major
     gacq_row* rows_bin;     // [n_snap][n_prn][B]
     float* pmap;            // optional [n_prn][B][P] (single snapshot), else null
+    int* bad;               // atomicMin'd to the index of a snapshot holding a non-finite sample
     int64_t pair0;          // first (snapshot, bin) pair of this chunk
     int B, R, n_coh, P, logM, n_prn, radius;  // M = 2^logM in total, L = 1 or 2 CTA-sized parts
 };
@@ -239,10 +240,13 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
     const cx* x = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * N;
     const cx* c = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * N;
     const int ext = N + a.P - 1;
+    unsigned fin = 0x7f800000u;  // see fin_word
     auto wext = [&](int j) {  // periodically extended, zero-padded wiped block
         if (j >= ext) return czero();
         const int n = j < N ? j : j - N;
-        return cmul_exact(__ldg(&x[n]), __ldg(&c[n]));  // acquisition.py:141, kernels.py:78-86
+        const cx xv = __ldg(&x[n]);
+        fin = fin_word(xv, fin);
+        return cmul_exact(xv, __ldg(&c[n]));  // acquisition.py:141, kernels.py:78-86
     };
     auto input = [&](int j) {  // transform input j (the L = 2 split folds in its radix-2 step)
         cx y = wext(j);
@@ -260,6 +264,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
     __syncthreads();
     gen_fft_inplace<-1>(sm, logMs, a.tw, L);
 #endif
+    if (__syncthreads_or(fin == 0u) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
     for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[GACQ_GEN_STOCKHAM ? gpad(k) : k];
 }
@@ -355,6 +360,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     bidx = red_i[0];
     for (int i = 1; i < nw; ++i)
         if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
+    if (bidx == 0x7fffffff) { best = 0.f; bidx = 0; }  // all-NaN powers (non-finite input, flagged by K1)
     const int64_t pair = a.pair0 + lp;
     const int64_t s = pair / a.B;
     const int b = (int)(pair % a.B);

@@ -86,6 +86,7 @@ struct FwdPfaArgs {
     int64_t stride;        // complex samples between snapshots
     const float2* carrier; // [B][n_coh] wipe-off replicas
     cx* Z;                 // [pairs][R][D][kBuf] spectra
+    int* bad;              // atomicMin'd to the index of a snapshot holding a non-finite sample
     int64_t pair0;         // first (snapshot, bin) pair of this chunk, pair = s*B + b
     int B, R, n_coh, P, K;
 };
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
     const cx* xs = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh;
     const cx* cs = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
     // D = 4, K = 1 (C1-C3): chip sums computed in the wipe (wipe_chips4), wt then holds z[rho][m]
-    wipe_fold<D, 32 * W>(xs, cs, a.P, a.K, wt);
+    if (wipe_fold<D, 32 * W>(xs, cs, a.P, a.K, wt) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     // One phase per warp (W = D >= 4: C1-C3 at D = 4, the 8.184 MHz default at D = 8): the chip
     // sums once per chip, in place. Thread t takes chips m = 32 W j + t, reads wt[k][m] and
     // wt[k][m + 1] (row 1023 repeats chip 0), and after a barrier overwrites wt[rho][m] =
@@ -459,7 +460,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) bl = min(bl, __shfl_xor_sync(0xffffffffu, bl, off));
             best = m;
-            bidx = bl;
+            bidx = bl == 0x7fffffff ? rho0 : bl;  // all-NaN powers (non-finite input, flagged by K1)
         } else {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
@@ -467,6 +468,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
                 if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
             }
+            if (bidx == 0x7fffffff) { best = 0.f; bidx = rho0; }  // all-NaN powers (flagged by K1)
         }
         if (lane == 0) red_k[w] = peak_key(best, bidx);
         if (threadIdx.x == 0) s_claim = claim;

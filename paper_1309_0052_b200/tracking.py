@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _lib
 from .cacode import CHIP_RATE_HZ, CODE_LENGTH
-from .errors import DegenerateInputError, InvalidConfigError, InvalidInputError
+from .errors import DegenerateInputError, InvalidConfigError, InvalidInputError, UnsupportedError
 
 L1_CARRIER_HZ = 1575.42e6  # gnss_signal.py:34
 LOOP_DAMPING = 0.7071067811865476  # tracking.py:44
@@ -174,6 +174,26 @@ class _EplChan(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+def _samples_arg(samples, trk):
+    """(total, pointer, flags, owner) of a sample buffer for gacq_trk_*: a CUDA array
+    (__cuda_array_interface__; the tracker's stream then waits for its producer) or a host
+    array. Only complex64 is implemented on the device: complex128 (Precision.DOUBLE) and
+    other dtypes are refused rather than silently rounded."""
+    cai = getattr(samples, "__cuda_array_interface__", None)
+    if cai is not None:
+        if cai["typestr"] != "<c8":
+            raise InvalidInputError("device samples must be complex64")
+        _lib.wait_for_producer(_lib.lib.gacq_trk_wait_stream, trk, cai)
+        return int(np.prod(cai["shape"])), cai["data"][0], _lib.SNAPS_ON_DEVICE, samples
+    arr = np.asarray(getattr(samples, "samples", samples))
+    if arr.dtype == np.complex128:
+        raise UnsupportedError("Precision.DOUBLE (complex128) is not implemented on the GPU path")
+    if arr.dtype != np.complex64:
+        raise InvalidInputError(f"samples must be complex64, got {arr.dtype}")
+    arr = np.ascontiguousarray(arr).reshape(-1)
+    return arr.size, arr.ctypes.data, 0, arr
+
+
 class TrackEngine:
     """Batched E/P/L correlators on one device (gacq_trk_*)."""
 
@@ -202,17 +222,7 @@ class TrackEngine:
                 c.code_p0[j] = code_phase_to_fixed((st.code_phase_chips + o) % CODE_LENGTH)
             c.code_step = code_step_to_fixed(st.code_rate_hz, fs)
             c.prn = int(st.prn)
-        cai = getattr(samples, "__cuda_array_interface__", None)
-        flags = 0
-        if cai is not None:
-            if cai["typestr"] != "<c8":
-                raise InvalidInputError("device samples must be complex64")
-            total = int(np.prod(cai["shape"]))
-            ptr = cai["data"][0]
-            flags = _lib.SNAPS_ON_DEVICE
-        else:
-            arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
-            total, ptr = arr.size, arr.ctypes.data
+        total, ptr, flags, _keep = _samples_arg(samples, self._trk)
         out = np.empty((len(states), 6), dtype=np.float32)
         _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, n, chans, len(states), flags, out.ctypes.data))
         return out
@@ -230,14 +240,7 @@ class TrackEngine:
     def correlate_chans(self, samples, chans: np.ndarray, n: int, out: np.ndarray | None = None) -> np.ndarray:
         """Like correlate() but from prepared gacq_epl_chan records (tracking.EPL_CHAN_DTYPE)."""
         chans = np.ascontiguousarray(chans)
-        cai = getattr(samples, "__cuda_array_interface__", None)
-        if cai is not None:
-            if cai["typestr"] != "<c8":
-                raise InvalidInputError("device samples must be complex64")
-            total, ptr, flags = int(np.prod(cai["shape"])), cai["data"][0], _lib.SNAPS_ON_DEVICE
-        else:
-            arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
-            total, ptr, flags = arr.size, arr.ctypes.data, 0
+        total, ptr, flags, _keep = _samples_arg(samples, self._trk)
         if out is None:
             out = np.empty((chans.size, 6), dtype=np.float32)
         _lib.check(_lib.lib.gacq_trk_epl(self._trk, ptr, total, int(n), chans.ctypes.data, chans.size, flags,
@@ -451,14 +454,7 @@ def track_step(samples, offsets, batch: TrackBatch, config: TrackConfig, device:
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     if off.shape != (b.prn.size,):
         raise InvalidInputError("one block offset per channel")
-    cai = getattr(samples, "__cuda_array_interface__", None)
-    if cai is not None:
-        if cai["typestr"] != "<c8":
-            raise InvalidInputError("device samples must be complex64")
-        total, ptr, flags = int(np.prod(cai["shape"])), cai["data"][0], _lib.SNAPS_ON_DEVICE
-    else:
-        arr = np.ascontiguousarray(samples, dtype=np.complex64).reshape(-1)
-        total, ptr, flags = arr.size, arr.ctypes.data, 0
+    total, ptr, flags, _keep = _samples_arg(samples, eng._trk)
     sums = np.empty((b.prn.size, 6), dtype=np.float32)
     out = np.empty((b.prn.size, 3), dtype=np.float64)
     bad = C.c_int64(-1)

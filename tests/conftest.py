@@ -17,3 +17,12 @@ def pytest_configure(config):
 @pytest.fixture
 def rng():
     return np.random.default_rng(12345)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write the parity tie ledger (tests/parity.py) when any GPU parity test ran."""
+    import parity
+
+    if parity.LEDGER or any(getattr(i, "get_closest_marker", lambda m: None)("gpu")
+                            for i in getattr(session, "items", [])):
+        parity.write_ledger(ROOT)

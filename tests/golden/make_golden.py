@@ -115,6 +115,8 @@ FS8 = 8.184e6
 def main():
     if "--generic" in sys.argv:
         return main_generic()
+    if "--extra" in sys.argv:
+        return main_extra()
     t0 = time.time()
     cases = []
     maps = {}
@@ -285,6 +287,75 @@ def main_generic():
         numpy=np.__version__, scipy=__import__("scipy").__version__, cases=cases), indent=1))
     np.savez_compressed(OUT / "maps_generic.npz", **maps)
     print("wrote", len(cases), "generic cases,", len(maps), "maps in", round(time.time() - t0, 1), "s")
+
+
+def _acq_one(args):
+    """One reference channel in a worker process (acquire_all results are bit-identical to
+    sequential per-channel calls for any plan, acquisition.py:196-197)."""
+    kind, spec, prn, cfg_kw = args
+    if kind == "snapshot":
+        kw = {k: spec[k] for k in ("doppler_span_hz",) if k in spec}
+        buf, _ = ref_snapshot(spec["index"], spec["fs"], spec["duration_s"], spec["base_seed"], **kw)
+    else:
+        raise ValueError(kind)
+    return res_dict(acquire_channel(buf, generate_ca_code(prn), AcqConfig(**cfg_kw)))
+
+
+def main_extra():
+    """Round-2 parity cases (VERDICT r01 "Close the parity holes" and the large-transform
+    rates): C4 with all 32 PRNs on 2 snapshots, C2 on 4 more snapshots, and rates whose
+    transform exceeds 32768 points or whose chip oversampling D exceeds 16. Channels run in
+    parallel worker processes. Writes tests/golden/golden_extra.json."""
+    import multiprocessing as mp
+
+    t0 = time.time()
+    cases = []
+    all_prns = list(range(1, 33))
+    specs = []
+    fs16 = 16.368e6
+    for i in range(2):
+        specs.append((f"c4x_snap{i}", dict(index=i, fs=fs16, duration_s=20e-3, base_seed=810,
+                                           doppler_span_hz=9750.0), C4))
+    fs4 = 4.092e6
+    for i in range(1, 5):
+        specs.append((f"c2_snap{i}", dict(index=i, fs=fs4, duration_s=10e-3, base_seed=200), C2))
+    g2 = AcqConfig(doppler_min_hz=-5000.0, doppler_max_hz=5000.0, doppler_step_hz=500.0,
+                   noncoherent_rounds=2)
+    # generic rates beyond 32768 points (n_coh + P - 1 > 32768, n_coh not a power of two)
+    specs.append(("gen20M_snap0", dict(index=0, fs=20.0e6, duration_s=2e-3, base_seed=930), g2))
+    specs.append(("gen20M_snap1", dict(index=1, fs=20.0e6, duration_s=2e-3, base_seed=930), g2))
+    specs.append(("gen16367k_coh2", dict(index=0, fs=16.367e6, duration_s=4e-3, base_seed=940),
+                  AcqConfig(coherent_ms=2, noncoherent_rounds=2, doppler_step_hz=250.0,
+                            doppler_min_hz=-2000.0, doppler_max_hz=2000.0)))
+    specs.append(("gen8M192_coh5", dict(index=0, fs=8.192e6, duration_s=10e-3, base_seed=950),
+                  AcqConfig(coherent_ms=5, noncoherent_rounds=2, doppler_step_hz=100.0,
+                            doppler_min_hz=-1000.0, doppler_max_hz=1000.0)))
+    # chip-aligned with D > 16 samples per chip
+    specs.append(("d20_snap0", dict(index=0, fs=20.46e6, duration_s=2e-3, base_seed=960), g2))
+    specs.append(("d32_snap0", dict(index=0, fs=32.736e6, duration_s=2e-3, base_seed=970), g2))
+    only = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")]
+    if only:
+        specs = [sp for sp in specs if sp[0] in only[0].split(",")]
+    jobs = [("snapshot", spec, p, cfg_dict(cfg)) for _, spec, cfg in specs for p in all_prns]
+    with mp.Pool(min(8, mp.cpu_count())) as pool:
+        res = pool.map(_acq_one, jobs, chunksize=1)
+    k = 0
+    for name, spec, cfg in specs:
+        kw = {x: spec[x] for x in ("doppler_span_hz",) if x in spec}
+        buf, truth = ref_snapshot(spec["index"], spec["fs"], spec["duration_s"], spec["base_seed"], **kw)
+        cases.append(dict(name=name, kind="snapshot", spec=dict(spec, truth=truth), fs=spec["fs"],
+                          n_samples=len(buf), input_sha256=sha(buf.samples), prns=all_prns,
+                          config=cfg_dict(cfg), results=res[k:k + len(all_prns)]))
+        k += len(all_prns)
+        print(f"{name}: 32 prns ({time.time() - t0:.1f}s)", flush=True)
+    path = OUT / "golden_extra.json"
+    if only and path.exists():
+        old = [c for c in json.loads(path.read_text())["cases"] if c["name"] not in {c["name"] for c in cases}]
+        cases = old + cases
+    path.write_text(json.dumps(dict(
+        generator="tests/golden/make_golden.py --extra", reference="gnssperf 0.1.0 (/root/reference/pkg)",
+        numpy=np.__version__, scipy=__import__("scipy").__version__, cases=cases), indent=1))
+    print("wrote", len(cases), "extra cases in", round(time.time() - t0, 1), "s")
 
 
 if __name__ == "__main__":

@@ -10,7 +10,10 @@ reference metric is within TIE_REL of the threshold.
 
 from __future__ import annotations
 
+import json
 import math
+import os
+from pathlib import Path
 
 METRIC_RTOL = 1e-4   # north_star: correlation peak values within 1e-4 relative (fp32)
 TIE_REL = 1e-5
@@ -45,3 +48,36 @@ def compare(got: dict, ref: dict, threshold: float, pmap=None, bins=None) -> str
         return "tie"
     return (f"cell ({got['doppler_hz']}, {got['code_phase_samples']}) vs "
             f"({ref['doppler_hz']}, {ref['code_phase_samples']}): oracle power {mine} vs peak {peak}")
+
+
+# ---- tie exemptions: named inputs only, every one recorded -------------------------------
+# (input name -> why its reference power map holds float32-indistinguishable top cells).
+# A test may accept a 'tie' verdict only for an input listed here; every accepted tie is
+# appended to LEDGER, which tests/conftest.py writes out at the end of the session
+# ($GACQ_TIE_LEDGER, default gpurun_out/parity_ties.json) so each run's exemption count is
+# on record.
+ALLOWED_TIES = {
+    "aligned_tie_0hz": "0 Hz truth on the default 8.184 MHz grid: the reference map holds an exact "
+                       "fp32 tie between the symmetric -333.3/+333.3 Hz bins (SURVEY.md 8(c))",
+    "gen5M_truth": "noise-free 5 MHz truth at -1750 Hz, exactly mid-bin: exact top-2 ties in the "
+                   "reference map (bins 6/7 for PRN 12, 1/12 for PRN 13)",
+}
+LEDGER: list = []
+
+
+def record(test: str, name: str, prn: int, verdict: str) -> None:
+    """Account for one verdict: a 'tie' must belong to an ALLOWED_TIES input."""
+    if verdict != "tie":
+        return
+    assert name in ALLOWED_TIES, f"{test}: tie on input {name!r} prn {prn} is not an allowed exemption"
+    LEDGER.append(dict(test=test, input=name, prn=int(prn), reason=ALLOWED_TIES[name]))
+
+
+def write_ledger(root: Path) -> Path:
+    path = Path(os.environ.get("GACQ_TIE_LEDGER") or root / "gpurun_out" / "parity_ties.json")
+    path.parent.mkdir(parents=True, exist_ok=True)
+    by_input: dict = {}
+    for t in LEDGER:
+        by_input[t["input"]] = by_input.get(t["input"], 0) + 1
+    path.write_text(json.dumps(dict(total=len(LEDGER), by_input=by_input, ties=LEDGER), indent=1))
+    return path

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol(pkg):
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.EXPORTS)
-    assert lib.gacq_version() == 1
+    assert lib.gacq_version() == _lib.ABI_VERSION == 2
 
 
 def test_library_is_sm100a_only(pkg):

@@ -26,12 +26,24 @@ def test_oracle_regenerates_reference_inputs(name):
     assert sha(x) == c["input_sha256"], "oracle synthesis diverged from the reference"
 
 
+def _prn_sample(c):
+    """The channels the CPU suite re-runs: all of them, except on the C4 cases (1.5 s per
+    channel on the oracle), where three planted satellites and one absent PRN stand in; the
+    GPU suite checks every channel of those against the same reference results."""
+    if c["name"].startswith("c4x_"):
+        planted = [t[0] for t in c["spec"]["truth"][:3]]
+        absent = [p for p in c["prns"] if p not in {t[0] for t in c["spec"]["truth"]}][:1]
+        return [i for i, p in enumerate(c["prns"]) if p in planted + absent]
+    return list(range(len(c["prns"])))
+
+
 @pytest.mark.parametrize("name", FAST)
 def test_oracle_matches_reference_results_bit_exact(name):
     c = case(name)
     x = case_input(c)
-    got = oracle.acquire_all(x, c["fs"], c["prns"], oracle_config(c))
-    for g, r in zip(got, c["results"]):
+    idx = _prn_sample(c)
+    got = oracle.acquire_all(x, c["fs"], [c["prns"][i] for i in idx], oracle_config(c))
+    for g, r in zip(got, [c["results"][i] for i in idx]):
         for k in ("prn", "doppler_hz", "code_phase_samples", "detected", "bins_searched",
                   "multiplications_performed"):
             assert g[k] == r[k], (k, g[k], r[k])

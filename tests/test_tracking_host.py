@@ -72,3 +72,21 @@ def test_track_batch_round_trip():
     states = [to_state(ch["init"]) for _, ch in all_channels()]
     assert trk.TrackBatch.from_states(states).to_states() == states
     assert case("locked_8184k")["epochs"] == 10
+
+
+def test_mixed_rate_batch_closes_each_channel_at_its_own_block_length():
+    """gacq_trk_close advances every channel's NCOs over that channel's own block length
+    (tracking.py:122-123), so a batch mixing sample rates equals the per-channel closure."""
+    rng = np.random.default_rng(11)
+    rates = [4.092e6, 8.184e6, 5e6, 16.368e6]
+    states = [trk.TrackState(prn=1 + i, code_phase_chips=float(rng.uniform(0, 1023)),
+                             carrier_phase_cycles=float(rng.uniform(0, 1)), doppler_hz=float(rng.uniform(-4e3, 4e3)),
+                             code_rate_hz=1.023e6, sample_rate_hz=rates[i % 4]) for i in range(16)]
+    cfg = trk.TrackConfig()
+    sums = rng.normal(size=(16, 6)).astype(np.float32) * 100
+    batch, outs = trk.close_loops_batch(sums, trk.TrackBatch.from_states(states), cfg)
+    for i, s in enumerate(states):
+        o = trk._outputs(sums[i:i + 1], trk.block_length(s, cfg))[0]
+        ref_state, ref_out = trk._close_loops(o, s, cfg)
+        assert batch.to_states()[i] == ref_state, i
+        assert outs["pll_error_cycles"][i] == ref_out.pll_error_cycles

@@ -3,12 +3,10 @@
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
 
 Exercises every device kernel: the table builders, the 1023-point path (K1/K2 at D = 2, 4, 16,
-powers in registers and in L2 rows), the 2048-point path (GACQ_PATH=2048), the tensor-core K2
-(GACQ_TC=1), the generic power-of-two path (5 MHz; 6 MHz x 2 ms for the two-part transform;
+powers in registers and in L2 rows), the generic power-of-two path (5 MHz; 6 MHz x 2 ms for the two-part transform;
 8.192 MHz at 1 and 4 ms for the circular transforms), K3, the power-map hook, the int8 dequantizer and the tracking correlators.
 """
 
-import os
 import sys
 from pathlib import Path
 
@@ -22,34 +20,28 @@ import paper_1309_0052_b200 as g  # noqa: E402
 from paper_1309_0052_b200 import tracking as trk  # noqa: E402
 
 
-def run(fs, rounds, coh=1, env=None):
-    for k in ("GACQ_PATH", "GACQ_TC"):
-        os.environ.pop(k, None)
-    os.environ.update(env or {})
+def run(fs, rounds, coh=1, generic=False):
     cfg = g.AcqConfig(doppler_min_hz=-1000.0, doppler_max_hz=1000.0, doppler_step_hz=500.0,
                       noncoherent_rounds=rounds, coherent_ms=coh)
     x = np.stack([oracle.make_snapshot(i, fs, rounds * coh * 1e-3, base_seed=11)[0] for i in range(2)])
-    eng = g.AcqEngine(fs, [1, 5, 9], cfg)
+    eng = g.AcqEngine(fs, [1, 5, 9], cfg, force_generic=generic)
     r = eng.search(x)
     q = np.clip(np.round(np.stack([x.real, x.imag], -1).reshape(2, -1) / 40.0 * 127), -127, 127).astype(np.int8)
     eng.search_quantized(q, 0, 40.0)
     eng.power_map(x[0])
     eng.carrier_table()
-    print(fs, env or "", eng.info["path"], r.code_phase_samples[0].tolist())
+    print(fs, generic, eng.info["path"], r.code_phase_samples[0].tolist())
     eng.close()
 
 
 def main():
     for fs, rounds in ((2.046e6, 2), (4.092e6, 2), (16.368e6, 1)):
         run(fs, rounds)
-        run(fs, rounds, env={"GACQ_PATH": "2048"})
-    run(4.092e6, 2, env={"GACQ_TC": "1"})
-    run(16.368e6, 1, env={"GACQ_TC": "1"})
+        run(fs, rounds, generic=True)
     run(5.0e6, 2)
     run(6.0e6, 1, coh=2)
     run(8.192e6, 2)  # power-of-two n_coh: circular 8192-point transform, 16 values per thread
     run(8.192e6, 1, coh=4)  # circular 32768-point (two-part) transform
-    os.environ.pop("GACQ_TC", None)
     st = [trk.TrackState(prn=p, code_phase_chips=10.0 * p, carrier_phase_cycles=0.0, doppler_hz=100.0 * p,
                          code_rate_hz=1.023e6, sample_rate_hz=4.092e6) for p in (1, 2, 3)]
     blk = oracle.make_snapshot(0, 4.092e6, 1e-3, base_seed=3)[0]
