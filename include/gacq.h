@@ -255,6 +255,10 @@ int gacq_trk_step(gacq_trk* trk, const void* blocks, int64_t total_samples, cons
                   gacq_trk_batch* batch, const gacq_trk_config* cfg, uint32_t flags, float* sums, double* out,
                   int64_t* bad_channel);
 
+/* Measured FP32 peak of `device` in TFLOP/s (packed FFMA2 chains, the codelets' instruction
+ * form): the denominator bench.py reports beside the nominal 148 x 128 x 2 x clock. */
+int gacq_fp32_probe(int32_t device, double* tflops);
+
 /* Page-locked host buffers for overlapped H2D (cudaHostAlloc / cudaFreeHost). */
 int gacq_host_alloc(int64_t bytes, void** out);
 int gacq_host_free(void* ptr);

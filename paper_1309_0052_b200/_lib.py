@@ -70,7 +70,7 @@ EXPORTS = ("gacq_version", "gacq_last_error", "gacq_create", "gacq_info_get", "g
            "gacq_run", "gacq_run_quantized", "gacq_power_map", "gacq_stats_get", "gacq_stats_reset",
            "gacq_host_alloc", "gacq_host_free", "gacq_ca_code", "gacq_trk_create", "gacq_trk_destroy",
            "gacq_trk_epl", "gacq_carrier_table", "gacq_synth", "gacq_trk_close", "gacq_trk_chans", "gacq_trk_step",
-           "gacq_wait_stream", "gacq_trk_wait_stream")
+           "gacq_wait_stream", "gacq_trk_wait_stream", "gacq_fp32_probe")
 FMT_INT8, FMT_INT16 = 0, 1
 
 
@@ -109,6 +109,7 @@ def _load() -> C.CDLL:
                                  C.c_void_p]
     lib.gacq_wait_stream.argtypes = [C.c_void_p, C.c_void_p]
     lib.gacq_trk_wait_stream.argtypes = [C.c_void_p, C.c_void_p]
+    lib.gacq_fp32_probe.argtypes = [C.c_int32, C.POINTER(C.c_double)]
     if lib.gacq_version() != ABI_VERSION:
         raise ImportError("libgacq ABI version mismatch")
     return lib

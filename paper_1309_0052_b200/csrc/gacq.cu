@@ -114,7 +114,6 @@ struct gacq_ctx {
     int device = 0;
     double fs = 0;
     int n_coh = 0, P = 0, D = 0, K = 0, R = 0, B = 0, n_prn = 0, radius = 0;
-    int cw = 4, cpw = 1;  // PFA K2: warps per CTA, phases per warp
     float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kCcHalf]
     bool gen = false;         // generic power-of-two path (rates that are not chip-aligned)
     int logM = 0;             // its transform length M = 2^logM >= n_coh + P - 1
@@ -135,7 +134,7 @@ struct gacq_ctx {
     gacq_row* d_rows = nullptr;
     int64_t rows_cap = 0;
     float* d_pmap = nullptr;
-    float* d_row_scratch = nullptr;  // [corr_slots][D*1024] power rows when D > 4
+    float* d_prow = nullptr;         // K2 per-phase power rows [corr_slots][kCorrWarps][D][kPhaseRow]
     int64_t corr_slots = 0;          // resident K2 CTAs (persistent grid)
     unsigned long long* d_counter = nullptr;  // K2 work counter
     int* d_bad = nullptr;   // lowest snapshot index holding a non-finite sample (K1 atomicMin)
@@ -195,24 +194,9 @@ cudaError_t launch_fwd_pfa(const gacq_ctx* c, const FwdPfaArgs& fa, int64_t bloc
     return cudaErrorInvalidConfiguration;
 }
 
-// K2 shape: PW phases per warp, W = ceil(D/PW) <= 6 warps; among the two smallest feasible
-// PW take the one with the least idle phase slots (W PW - D), ties -> more warps.
-void corr_pfa_shape(int D, int* W, int* PW) {
-    const int p0 = (D + kCorrMaxWarps - 1) / kCorrMaxWarps;
-    int best_pw = p0, best_w = (D + p0 - 1) / p0;
-    const int w1 = (D + p0) / (p0 + 1);
-    if (w1 * (p0 + 1) < best_w * best_pw) { best_pw = p0 + 1; best_w = w1; }
-    *W = best_w;
-    *PW = best_pw;
-}
-
 cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
-    const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_items);
-    if (ca.n_items + c->corr_slots >= INT32_MAX) return cudaErrorInvalidValue;  // 32-bit item indices
-    if (c->cpw == 1)
-        gacq_corr_pfa_kernel<true><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
-    else
-        gacq_corr_pfa_kernel<false><<<(unsigned)blocks, 32 * c->cw, corr_pfa_smem(c->cw), c->stream>>>(ca);
+    const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_units);
+    gacq_corr_pfa_kernel<<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
     return cudaGetLastError();
 }
 
@@ -367,8 +351,10 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
                 gacq_gen_corr_kernel<1, 32><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
         } else {
-            CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_row_scratch, p0,
-                           np * c->n_prn, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, c->cpw, 0,
+            const int64_t n_units = (np + kCorrWarps - 1) / kCorrWarps * c->n_prn;
+            if (n_units + c->corr_slots >= INT32_MAX) return fail(GACQ_ERR_UNSUPPORTED, "chunk too large");
+            CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_prow, p0, (int)np,
+                           (int)n_units, c->d_counter, c->B, c->R, c->D, c->P, c->n_prn, c->radius, 0,
                            (unsigned)(((1ull << 32) + c->D - 1) / c->D)};
             CUDA_TRY(launch_corr_pfa(c, ca));
         }
@@ -437,7 +423,7 @@ void destroy_ctx(gacq_ctx* c) {
         cudaFree(c->d_rows_bin);
         cudaFree(c->d_rows);
         cudaFree(c->d_pmap);
-        cudaFree(c->d_row_scratch);
+        cudaFree(c->d_prow);
         cudaFree(c->d_counter);
         cudaFree(c->d_bad);
         if (c->h_bad) cudaFreeHost(c->h_bad);
@@ -535,7 +521,6 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->radius = p->exclusion_radius_samples ? p->exclusion_radius_samples : (int)std::ceil(fs / kChipRate);
     c->gen = gen;
     c->logM = logM;
-    if (!gen) corr_pfa_shape(D, &c->cw, &c->cpw);
     c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
     c->prns.assign(p->prns, p->prns + p->n_prn);
 
@@ -644,10 +629,11 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, corr1_max));
         CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
     }
-    const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * kBuf) *
+    const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * kSpec) *
                                (int64_t)sizeof(float2);
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
+    if (!gen && c->z_pairs > kCorrWarps) c->z_pairs -= c->z_pairs % kCorrWarps;  // whole K2 pair groups per chunk
     CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
     CTX_TRY(cudaMalloc(&c->d_bad, sizeof(int)));
     CTX_TRY(cudaHostAlloc(&c->h_bad, sizeof(int), cudaHostAllocPortable));
@@ -657,26 +643,20 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     }
     {
         // every PFA variant gets the largest dynamic shared memory any plan launches it with
-        CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     corr_pfa_smem(kCorrMaxWarps)));
-        CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     corr_pfa_smem(kCorrMaxWarps)));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     corr_pfa_smem()));
+        CTX_TRY(cudaFuncSetAttribute(gacq_corr_pfa_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 #define GACQ_ATTR_FWDP(DD, WW)                                                                             \
     CTX_TRY(cudaFuncSetAttribute(gacq_fwd_pfa_kernel<DD, WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                  fwd_pfa_smem(DD, WW)));
         GACQ_PFA_FWD_VARIANTS(GACQ_ATTR_FWDP)
 #undef GACQ_ATTR_FWDP
         int per_sm = 0, sms = 0;
-        if (c->cpw == 1)
-            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<true>, 32 * c->cw,
-                                                                  corr_pfa_smem(c->cw)));
-        else
-            CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<false>, 32 * c->cw,
-                                                                  corr_pfa_smem(c->cw)));
+        CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel, 32 * kCorrWarps,
+                                                              corr_pfa_smem()));
         CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
         c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
-        if (c->cpw > 1)
-            CTX_TRY(cudaMalloc(&c->d_row_scratch, (size_t)c->corr_slots * c->D * kChips * sizeof(float)));
+        CTX_TRY(cudaMalloc(&c->d_prow, (size_t)c->corr_slots * kCorrWarps * c->D * kPhaseRow * sizeof(float)));
         CTX_TRY(cudaMalloc(&c->d_counter, sizeof(unsigned long long)));
     }
 #undef CTX_TRY
@@ -831,6 +811,64 @@ int gacq_synth(int32_t device, double fs, int64_t n_snap, int64_t n, int32_t n_s
     cudaFree(d_chips);
     if (stream) cudaStreamDestroy(stream);
     if (e != cudaSuccess) return fail(GACQ_ERR_CUDA, "gacq_synth failed: %s", cudaGetErrorString(e));
+    return GACQ_OK;
+}
+
+// Measured FP32 roof for the roofline denominator (MEASURED_PEAKS.json has no FP32 entry):
+// 16 independent packed FFMA2 chains per thread with broadcast coefficients, 8 warps per SM
+// block x 4 blocks per SM, the instruction form the transform codelets use.
+__global__ void gacq_fp32_probe_kernel(float* out, int iters, float s) {
+    cx acc[16], x[4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = pk(threadIdx.x * 1e-3f + i, (float)i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = pk(s * i, s + i);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc[k] = fma2(x[j], bc(0.125f * (k + 1) + 0.01f * j), acc[k]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = acc[j] ^ (cx)(it & 1);
+    }
+    cx r = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r ^= acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (float)(r & 0xffff);
+}
+
+int gacq_fp32_probe(int32_t device, double* tflops) {
+    if (!tflops) return fail(GACQ_ERR_INVALID, "null argument");
+    DeviceGuard g(device);
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    const int threads = 256, blocks = 4 * sms, iters = 4096;
+    float* out = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto work = [&]() -> cudaError_t {
+        cudaError_t e;
+        if ((e = cudaMalloc(&out, sizeof(float) * blocks * threads)) || (e = cudaEventCreate(&e0)) ||
+            (e = cudaEventCreate(&e1)))
+            return e;
+        float best = 1e30f;
+        for (int rep = 0; rep < 4; ++rep) {
+            cudaEventRecord(e0);
+            gacq_fp32_probe_kernel<<<blocks, threads>>>(out, iters, 1.0001f);
+            cudaEventRecord(e1);
+            if ((e = cudaEventSynchronize(e1))) return e;
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (rep > 0) best = std::min(best, ms);
+        }
+        // 64 FFMA2 per iteration, 4 flops per lane each
+        *tflops = (double)blocks * threads * iters * 64.0 * 4.0 / (best * 1e-3) / 1e12;
+        return cudaGetLastError();
+    };
+    const cudaError_t e = work();
+    cudaFree(out);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (e != cudaSuccess) return fail(GACQ_ERR_CUDA, "fp32 probe failed: %s", cudaGetErrorString(e));
     return GACQ_OK;
 }
 

@@ -22,20 +22,21 @@
 
 namespace gacq {
 
-constexpr int kBuf = 33 * 32;                    // spectrum [k2][32]; column 31 is padding
+constexpr int kBuf = 33 * 32;                    // K1 exchange tile [k1][33] (+ padding)
 constexpr int kScr = 34;                         // K1 coop31 scratch (33 used; keeps 16 B alignment)
-constexpr unsigned kSpecBytes = kBuf * sizeof(cx);
-constexpr int kCorrMaxWarps = 6;
-constexpr int kCorrWarpCx = 2 * kBuf;            // per-warp shared memory (cx): two spectra
-constexpr int kCcHalf = 17 * 32;                 // Hermitian half of a conj code spectrum (cx)
-#ifndef GACQ_RADER31
-#define GACQ_RADER31 1                           // K2's 31-point stage by Rader's algorithm (rader31.cuh)
-#endif
+constexpr int kSpec = 1024;                      // one spectrum in HBM and in K2's buffer: [k2][31] + 1 pad
+constexpr unsigned kSpecBytes = kSpec * sizeof(cx);
+constexpr int kXch = 1023 + 33;                  // K2 exchange [q2][31] + coop31 scratch
+constexpr int kCcHalf = 17 * 31 + 1;             // Hermitian half [k2 <= 16][31] of a conj code spectrum (+ pad)
+constexpr int kCorrWarps = 4;                    // K2 warps per CTA (one item each)
+constexpr int kPhaseRow = 33 * 32;               // K2 scratch row of one phase: [q1 or coop slot][lane] floats
 #ifndef GACQ_PFA_MAXNREG
 #define GACQ_PFA_MAXNREG 168                     // 3 CTAs x 4 warps per SM; no spills (streamed stages)
 #endif
 
-__host__ __device__ constexpr int corr_pfa_smem(int W) { return W * (kCorrWarpCx * 8 + 16) + kCcHalf * 8; }
+// K2 dynamic smem: per warp a spectrum buffer and an exchange buffer, two code-spectrum slots
+// per CTA, one mbarrier per warp (3 CTAs per SM fit the 228 KB)
+__host__ __device__ constexpr int corr_pfa_smem() { return kCorrWarps * (kSpec + kXch) * 8 + 2 * kCcHalf * 8 + kCorrWarps * 8; }
 // K1 with one phase per warp (W == D) computes every chip sum before any warp writes its
 // exchange tile, so the exchange tiles alias the wiped-block table (one barrier in between)
 __host__ __device__ constexpr bool fwd_pfa_alias(int D, int W) { return W == D; }
@@ -54,6 +55,16 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // lane after the warp's generic accesses of `dst` (ordered by a __syncwarp before the call).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// the same copy into a buffer that only the async proxy ever writes and the generic proxy only
+// reads (reads already consumed, ordered by a __syncwarp): no proxy fence needed
+__device__ __forceinline__ void bulk_load_nofence(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -85,7 +96,7 @@ struct FwdPfaArgs {
     const float2* snaps;   // batch base (device), snapshot s at snaps + s*stride
     int64_t stride;        // complex samples between snapshots
     const float2* carrier; // [B][n_coh] wipe-off replicas
-    cx* Z;                 // [pairs][R][D][kBuf] spectra
+    cx* Z;                 // [pairs][R][D][kSpec] spectra
     int* bad;              // atomicMin'd to the index of a snapshot holding a non-finite sample
     int64_t pair0;         // first (snapshot, bin) pair of this chunk, pair = s*B + b
     int B, R, n_coh, P, K;
@@ -244,13 +255,13 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
                        [&](int, int k1, cx v) { T[k1 * 33 + 32] = v; });
         }
         __syncwarp();
-        // 33-point stage over n2 -> Z[k2][k1], coalesced 256 B stores
+        // 33-point stage over n2 -> Z[k2][k1] (rows of 31, the spectrum dense in 8184 B)
         if (lane < 31) {
             cx y[33];
 #pragma unroll
             for (int n2 = 0; n2 < 33; ++n2) y[n2] = T[lane * 33 + n2];
-            cx* dst = a.Z + (((int64_t)lp * a.R + rd) * D + rho) * kBuf + lane;
-            dft33<-1>(y, [&](int k2, cx v) { dst[k2 * 32] = v; });
+            cx* dst = a.Z + (((int64_t)lp * a.R + rd) * D + rho) * kSpec + lane;
+            dft33<-1>(y, [&](int k2, cx v) { dst[k2 * 31] = v; });
         }
         __syncwarp();
     }
@@ -258,15 +269,16 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
 
 // ---- K2 ---------------------------------------------------------------------------------
 struct CorrPfaArgs {
-    const cx* Z;           // spectra of this chunk, [pairs][R][D][kBuf]
-    const cx* Cc;          // [n_prn][kCcHalf] conj code spectra / 1023, rows k2 <= 16 of [k2][32]
+    const cx* Z;           // spectra of this chunk, [pairs][R][D][kSpec]
+    const cx* Cc;          // [n_prn][kCcHalf] conj code spectra / 1023, rows k2 <= 16 of [k2][31]
     gacq_row* rows_bin;    // [n_snap][n_prn][B]
     float* pmap;           // optional [n_prn][B][P] power map (single snapshot), else null
-    float* row_scratch;    // [gridDim][D][1023] native-order power rows when PW > 1
+    float* rows;           // [gridDim][kCorrWarps][D][kPhaseRow] per-phase power rows of the warp's item
     int64_t pair0;
-    int64_t n_items;       // pairs_in_chunk * n_prn, item = lp * n_prn + pi
+    int n_pairs;           // pairs in this chunk
+    int n_units;           // ceil(n_pairs / kCorrWarps) * n_prn; unit = group * n_prn + prn index
     unsigned long long* counter;  // zeroed before the launch
-    int B, R, D, P, n_prn, radius, PW;
+    int B, R, D, P, n_prn, radius;
     int zero;              // 0 (an opaque runtime zero, see dft31_stream)
     unsigned dmagic;       // ceil(2^32 / D): x / D == umulhi(x, dmagic) for x < 2^32 / D
 };
@@ -277,277 +289,226 @@ __device__ __forceinline__ int cell_q(int q1, int q2) {
     return q >= 2 * kChips ? q - 2 * kChips : q >= kChips ? q - kChips : q;
 }
 __device__ __forceinline__ bool better(float v, int l, float bv, int bl) { return v > bv || (v == bv && l < bl); }
-// (power >= 0, lag >= 0) as one unsigned key ordered like better(): the bits of a non-negative
-// float order like its value, and the low word inverts the lag so ties go to the lowest lag
-__device__ __forceinline__ unsigned long long peak_key(float v, int lag) {
-    return ((unsigned long long)__float_as_uint(v) << 32) | (0xffffffffu - (unsigned)lag);
-}
 __device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
     int d = abs(lag - peak);
     d = min(d, P - d);
     return d <= radius;
 }
 
-// Persistent: gridDim.x = resident CTA slots of 32 W threads; CTA c starts with item c and
-// claims the following items in order from a global counter (two items ahead, so the atomic
-// never stalls), so the CTAs sharing a pair's spectra run together and hit them in L2.
-// Warp w owns phases [w PW, w PW + PW) of the item. The item's conjugate code spectrum sits in
-// shared memory as the Hermitian half [17][32] (rows k2 > 16 are conj of row 33 - k2, lane
-// (31 - k1) mod 31), refilled with cp.async between items.
-// kRegs (PW == 1): the powers stay in registers through the argmax and the floor.
-// dynamic smem: corr_pfa_smem(W).
-template <bool kRegs>
+// Persistent, one item per warp: a CTA of kCorrWarps warps takes a unit = (group of kCorrWarps
+// consecutive (snapshot, bin) pairs, PRN) and warp w searches pair w of the group for that PRN
+// over all D phases and R rounds; the CTA's warps share the PRN's conjugate code spectrum in
+// shared memory (two slots: the next unit's lands with cp.async while this one runs). Units are
+// claimed in order from a global counter one ahead, so the n_prn CTAs sharing a group's spectra
+// run together and read them from L2.
+//
+// Per transform (phase rho, round r) of a warp: the spectrum Z (8184 B) sits in the warp's buffer
+// (cp.async.bulk + mbarrier); every lane k1 < 31 loads its column and the code spectrum at once,
+// Y = Z * Cc, the 3-point layer of the 33-point stage -- after which the buffer is free and lane 0
+// issues the bulk copy of the warp's next spectrum into it (no generic-proxy write ever touches
+// that buffer, so it needs no proxy fence) -- then the 11-point layers write the exchange buffer
+// E[q2][31], the 31-point stage over k1 (lane = q2, Rader) and the spread row q2 = 32 (coop31),
+// and |g|^2 accumulated in registers over the rounds.
+// After the R rounds of a phase its powers go to the warp's scratch row in global memory (L2)
+// and its first argmax (value desc, lag asc) into a running per-lane best. After the last phase
+// the warp reduces the peak and takes the exclusion floor from the scratch rows: only cells within
+// `radius` of the peak are excluded, and every lane owns at most one q per window (its q values
+// are congruent mod 33), found directly by the inverse map (q1, q2) = (16 q mod 31, 16 q mod 33).
+// acquisition.py:151-159.
 __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
-    __shared__ unsigned long long red_k[kCorrMaxWarps];  // per-warp (peak, lag) keys, see peak_key
-    __shared__ float red_f[kCorrMaxWarps];
-    __shared__ long long s_claim, s_claim0;  // s_claim0: the first claim (read before the item loop)
-    __shared__ float s_coef[15][32];  // coop31 columns, read conflict-free as s_coef[j-1][lane]
+    __shared__ int s_unit[2];
     extern __shared__ __align__(16) cx smem[];
-    const int W = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 15 * 32; i += blockDim.x) s_coef[i >> 5][i & 31] = coop31_coef(i & 31, (i >> 5) + 1);
-    cx* buf = smem + w * kCorrWarpCx;  // buf[0..kBuf), buf[kBuf..2kBuf)
-    cx* ccs = smem + W * kCorrWarpCx;  // [17][32] conj code spectrum half of the current item
-    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(ccs + kCcHalf) + 2 * w;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    cx* zbuf = smem + w * (kSpec + kXch);   // the warp's spectrum buffer (async proxy only)
+    cx* E = zbuf + kSpec;                   // exchange [q2][31] + coop31 scratch at E[1023..1055]
+    cx* ccs0 = smem + kCorrWarps * (kSpec + kXch);
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(ccs0 + 2 * kCcHalf) + w;
     if (lane == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        mbar_init(mbar, 1);
         fence_mbar_init();
     }
-    // item indices fit 32 bits (launch_corr_pfa checks): unsigned 32-bit divisions per item
-    const int n_items = (int)a.n_items;
     const unsigned n_prn = (unsigned)a.n_prn;
-    int item = blockIdx.x;
-    if (item >= n_items) return;
-    auto load_cc = [&](int it) {  // cp.async of the half spectrum of item `it`'s PRN
-        const char* g = reinterpret_cast<const char*>(a.Cc + ((unsigned)it % n_prn) * kCcHalf);
-        for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(ccs + 2 * i, g + 16 * i);
+    const int D = a.D, R = a.R;
+    int unit = blockIdx.x;
+    if (unit >= a.n_units) return;
+    const int64_t pair_span = (int64_t)R * D * kSpec;
+    auto load_cc = [&](int u, int slot) {  // cp.async of the half spectrum of unit u's PRN
+        const char* g = reinterpret_cast<const char*>(a.Cc + ((unsigned)u % n_prn) * kCcHalf);
+        cx* dst = ccs0 + slot * kCcHalf;
+        for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(dst + 2 * i, g + 16 * i);
         cp_async_commit();
     };
-    if (threadIdx.x == 0) s_claim0 = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
-    load_cc(item);
-
-    const int rho0 = w * a.PW;
-    const int nph = min(a.PW, a.D - rho0);  // phases of this warp
-    const int64_t pair_span = (int64_t)a.R * a.D * kBuf;
-    auto zbase = [&](int it) { return a.Z + (int64_t)((unsigned)it / n_prn) * pair_span + rho0 * kBuf; };
-    unsigned t = 0;  // this warp's transform count: buffer t & 1, mbarrier parity (t >> 1) & 1
-    __syncwarp();
-    if (lane == 0) bulk_load(buf, zbase(item), kSpecBytes, &mbar[0]);
-    float* rows = a.row_scratch + (int64_t)blockIdx.x * a.D * kChips;
-    const int pl = lane == 0 ? 0 : 31 - lane;  // Hermitian partner column of k1 = lane
+    auto pair_of = [&](int u) { return (int)((unsigned)u / n_prn) * kCorrWarps + w; };  // this warp's pair
+    if (threadIdx.x == 0) s_unit[1] = (int)(gridDim.x + atomicAdd(a.counter, 1ull));
+    load_cc(unit, 0);
+    {
+        const int lp = pair_of(unit);
+        __syncwarp();
+        if (lane == 0 && lp < a.n_pairs) bulk_load(zbuf, a.Z + lp * pair_span, kSpecBytes, mbar);
+    }
     cp_async_wait_all();
     __syncthreads();
-    int next = (int)s_claim0;  // s_claim itself is rewritten by thread 0 at the end of the first item
+    float* rows = a.rows + ((int64_t)blockIdx.x * kCorrWarps + w) * D * kPhaseRow;
+    const int pl = lane == 0 ? 0 : 31 - lane;  // Hermitian partner column of k1 = lane
+    const bool x0 = lane >= 1 && lane <= 16, x1 = lane >= 1 && lane <= 15;  // lanes owning coop cells
+    unsigned t = 0;  // transforms of this warp: mbarrier parity t & 1
 
-    for (;;) {
-        long long claim = 0;
-        if (threadIdx.x == 0 && next < n_items) claim = (long long)gridDim.x + (long long)atomicAdd(a.counter, 1ull);
-        const unsigned lp = (unsigned)item / n_prn;
-        const int pi = (int)((unsigned)item - lp * n_prn);
-        const cx* zb = a.Z + (int64_t)lp * pair_span + rho0 * kBuf;
-        const cx* zn = next < n_items ? zbase(next) : nullptr;
-
-        float best = -1.f;
-        int bidx = 0x7fffffff;
-        float acc[31], accx[2];
-        int rd = 0, ph = 0;  // round and phase of the current transform
+    for (int k = 0;; ++k) {
+        const int nxt = s_unit[(k + 1) & 1];
+        if (nxt < a.n_units) load_cc(nxt, (k + 1) & 1);  // its slot was last read in unit k - 1
+        if (threadIdx.x == 0) s_unit[k & 1] = nxt < a.n_units ? (int)(gridDim.x + atomicAdd(a.counter, 1ull)) : a.n_units;
+        const cx* ccs = ccs0 + (k & 1) * kCcHalf;
+        const int lp = pair_of(unit), pi = (int)((unsigned)unit % n_prn);
+        const int lpn = nxt < a.n_units ? pair_of(nxt) : a.n_pairs;  // the warp's next item
+        const cx* znext = lpn < a.n_pairs ? a.Z + lpn * pair_span : nullptr;
+        if (lp < a.n_pairs) {
+            const cx* zb = a.Z + lp * pair_span;
+            const int64_t pair = a.pair0 + lp;
+            const int b = (int)(pair % a.B);
+            float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
+            float best = -1.f;
+            int bidx = 0x7fffffff;
+            const int64_t rstep = (int64_t)D * kSpec;  // next round, same phase
 #pragma unroll 1
-        for (;; ++t) {
-            if (rd == 0) {
+            for (int rho = 0; rho < D; ++rho) {
+                const cx* cur = zb + rho * kSpec;
+                float acc[31], accx[2];
 #pragma unroll
                 for (int i = 0; i < 31; ++i) acc[i] = 0.f;
                 accx[0] = accx[1] = 0.f;
-            }
-            const bool last_rd = rd + 1 == a.R;
-            const bool last = last_rd && ph + 1 == nph;
-            if (lane == 0) {  // prefetch the warp's next spectrum into the other buffer
-                const cx* nsrc = !last ? zb + ((last_rd ? 0 : rd + 1) * a.D + (last_rd ? ph + 1 : ph)) * kBuf : zn;
-                if (nsrc) bulk_load(buf + ((t + 1) & 1) * kBuf, nsrc, kSpecBytes, &mbar[(t + 1) & 1]);
-            }
-            mbar_wait(&mbar[t & 1], (t >> 1) & 1);
-            cx* E = buf + (t & 1) * kBuf;
-            // Z * Cc and the 33-point stage over k2; results E[q2][k1] written in place
-            // (the 33-point stage reads all of E before the __syncwarp and writes after it)
-            if (lane < 31) {
-                const cx* Ec = E + lane;
-                dft33_stream<1>(
-                    [&](int k2, int dep) {
-                        // k2 is a compile-time constant here: the branch folds away
-                        return k2 <= 16 ? cmul(Ec[k2 * 32 + dep], ccs[k2 * 32 + lane + dep])
-                                        : cmul_conj(Ec[k2 * 32 + dep], ccs[(33 - k2) * 32 + pl + dep]);
-                    },
-                    a.zero, [&](int q2, cx v) {
-                        if (q2 == 0) __syncwarp(0x7fffffffu);
-                        E[q2 * 31 + lane] = v;
-                    });
-            }
-            __syncwarp();
-            // 31-point stage over k1 for row q2 = lane (+ row 32 spread over the warp, with its
-            // scratch in the buffer's unused tail E[1023..1055])
-            const cx e = lane < 31 ? E[32 * 31 + lane] : czero();
-            const cx* Er = E + lane * 31;
-#if GACQ_RADER31
-            dft31_rader_inv([&](int k1) { return Er[k1]; }, [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
-#else
-            dft31_stream<1>([&](int k1, int dep) { return Er[k1 + dep]; }, a.zero,
-                            [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+#pragma unroll 1
+                for (int rd = 0; rd < R; ++rd, ++t) {
+                    // the warp's next spectrum: next round, else the next phase's first round, else
+                    // the first spectrum of its next item
+                    const cx* nsrc = rd + 1 < R ? cur + rstep : rho + 1 < D ? zb + (rho + 1) * kSpec : znext;
+                    cur += rstep;
+#ifndef GACQ_ABL_NOWAIT
+                    mbar_wait(mbar, t & 1);
 #endif
-            coop31<1>(e, lane, [&](int j) { return s_coef[j - 1][lane]; }, E + kChips,
-                      [&](int sl, int, cx v) { accx[sl] = pow_acc(v, accx[sl]); });
-            __syncwarp();  // E is free for the prefetch issued at the next transform
-
-            if (!kRegs && last_rd) {  // phase done: spill to the row, track the argmax
-                const int rho = rho0 + ph;
-                float* row = rows + rho * kChips;
-#pragma unroll
-                for (int q1 = 0; q1 < 31; ++q1) {
-                    row[q1 * 33 + lane] = acc[q1];
-                    const int lag = a.D * cell_q(q1, lane) + rho;
-                    if (better(acc[q1], lag, best, bidx)) { best = acc[q1]; bidx = lag; }
+                    // Z * Cc and the 33-point stage over k2 (lanes k1 < 31); results E[q2][k1]
+                    if (lane < 31) {
+                        const cx* Ec = zbuf + lane;
+                        dft33_stream<1>(
+                            [&](int k2, int dep) {
+                                // k2 is a compile-time constant here: the branch folds away
+                                return k2 <= 16 ? cmul(Ec[k2 * 31 + dep], ccs[k2 * 31 + lane + dep])
+                                                : cmul_conj(Ec[k2 * 31 + dep], ccs[(33 - k2) * 31 + pl + dep]);
+                            },
+                            a.zero,
+                            [&]() {  // every input consumed: the buffer takes the next spectrum
+                                __syncwarp(0x7fffffffu);
+                                if (lane == 0 && nsrc) bulk_load_nofence(zbuf, nsrc, kSpecBytes, mbar);
+                            },
+                            [&](int q2, cx v) { E[q2 * 31 + lane] = v; });
+                    }
+                    __syncwarp();
+                    // 31-point stage over k1 for row q2 = lane (+ row 32 spread over the warp, its
+                    // scratch in E[1023..1055])
+                    const cx e = lane < 31 ? E[32 * 31 + lane] : czero();
+                    const cx* Er = E + lane * 31;
+                    dft31_rader_inv([&](int k1) { return Er[k1]; }, [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+                    coop31<1>(e, lane, [&](int j) { return __ldg(&kCoop31Coef[j - 1][lane]); }, E + kChips,
+                              [&](int sl, int, cx v) { accx[sl] = pow_acc(v, accx[sl]); });
+                    __syncwarp();  // E is free for the next transform
                 }
-                if (lane >= 1 && lane <= 16) {
+                // phase done: the row to scratch (and the parity power map), the running first argmax
+                float* row = rows + rho * kPhaseRow + lane;
 #pragma unroll
-                    for (int sl = 0; sl < 2; ++sl) {
-                        if (lane == 16 && sl == 1) break;
-                        const int q1 = lane == 16 ? 0 : sl ? 31 - lane : lane;
-                        row[q1 * 33 + 32] = accx[sl];
-                        const int lag = a.D * cell_q(q1, 32) + rho;
-                        if (better(accx[sl], lag, best, bidx)) { best = accx[sl]; bidx = lag; }
+                for (int q1 = 0; q1 < 31; ++q1) row[q1 * 32] = acc[q1];
+                row[31 * 32] = accx[0];
+                row[32 * 32] = accx[1];
+                if (pm) {
+#pragma unroll
+                    for (int q1 = 0; q1 < 31; ++q1) pm[D * cell_q(q1, lane) + rho] = acc[q1];
+                    if (x0) pm[D * cell_q(lane == 16 ? 0 : lane, 32) + rho] = accx[0];
+                    if (x1) pm[D * cell_q(31 - lane, 32) + rho] = accx[1];
+                }
+                // lane max (lanes without coop cells keep accx = 0, <= every power, never a lag
+                // candidate), then the lowest lag holding it, searched only when it can win
+                float m = acc[0];
+#pragma unroll
+                for (int q1 = 1; q1 < 31; ++q1) m = fmaxf(m, acc[q1]);
+                m = fmaxf(m, fmaxf(accx[0], accx[1]));
+                if (m >= best) {
+                    int bl = 0x7fffffff;
+                    unsigned mk = 0u;
+#pragma unroll
+                    for (int q1 = 0; q1 < 31; ++q1) mk |= (acc[q1] == m ? 1u : 0u) << q1;
+                    while (mk) {
+                        const int q1 = __ffs(mk) - 1;
+                        mk &= mk - 1u;
+                        bl = min(bl, D * cell_q(q1, lane) + rho);
+                    }
+                    if (x0 && accx[0] == m) bl = min(bl, D * cell_q(lane == 16 ? 0 : lane, 32) + rho);
+                    if (x1 && accx[1] == m) bl = min(bl, D * cell_q(31 - lane, 32) + rho);
+                    if (bl != 0x7fffffff && better(m, bl, best, bidx)) {
+                        best = m;
+                        bidx = bl;
                     }
                 }
             }
-            if (last) { ++t; break; }
-            if (last_rd) { rd = 0; ++ph; } else { ++rd; }
-        }
-        // cells of this lane (kRegs): (q1, lane) for q1 < 31, and coop cells
-        auto for_cells = [&](auto&& f) {
-#pragma unroll
-            for (int q1 = 0; q1 < 31; ++q1) f(acc[q1], a.D * cell_q(q1, lane) + rho0);
-            if (lane >= 1 && lane <= 15) {
-                f(accx[0], a.D * cell_q(lane, 32) + rho0);
-                f(accx[1], a.D * cell_q(31 - lane, 32) + rho0);
-            } else if (lane == 16) {
-                f(accx[0], a.D * cell_q(0, 32) + rho0);
-            }
-        };
-        // first argmax of the item (acquisition.py:151): ties -> lowest lag
-        const bool x0 = lane >= 1 && lane <= 16, x1 = lane >= 1 && lane <= 15;  // lanes owning coop cells
-        float lane_max = 0.f;
-        if (kRegs) {
-            // warp max of the values, then the lowest lag holding it (searched only by the lanes
-            // whose own max equals it). Lanes without coop cells keep accx = 0, which is <= every
-            // power and never a lag candidate.
-            float m = acc[0];
-#pragma unroll
-            for (int q1 = 1; q1 < 31; ++q1) m = fmaxf(m, acc[q1]);
-            m = fmaxf(m, fmaxf(accx[0], accx[1]));
-            lane_max = m;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-            int bl = 0x7fffffff;
-            if (lane_max == m) {  // cells equal to the max as a mask; lags only for its set bits
-                unsigned mk = 0u;
-#pragma unroll
-                for (int q1 = 0; q1 < 31; ++q1) mk |= (acc[q1] == m ? 1u : 0u) << q1;
-                while (mk) {
-                    const int q1 = __ffs(mk) - 1;
-                    mk &= mk - 1u;
-                    bl = min(bl, a.D * cell_q(q1, lane) + rho0);
-                }
-                if (x0 && accx[0] == m) bl = min(bl, a.D * cell_q(lane == 16 ? 0 : lane, 32) + rho0);
-                if (x1 && accx[1] == m) bl = min(bl, a.D * cell_q(31 - lane, 32) + rho0);
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) bl = min(bl, __shfl_xor_sync(0xffffffffu, bl, off));
-            best = m;
-            bidx = bl == 0x7fffffff ? rho0 : bl;  // all-NaN powers (non-finite input, flagged by K1)
-        } else {
+            // the item's first argmax (acquisition.py:151): value desc, lag asc, over the warp
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 const float ov = __shfl_xor_sync(0xffffffffu, best, off);
                 const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
                 if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
             }
-            if (bidx == 0x7fffffff) { best = 0.f; bidx = rho0; }  // all-NaN powers (flagged by K1)
-        }
-        if (lane == 0) red_k[w] = peak_key(best, bidx);
-        if (threadIdx.x == 0) s_claim = claim;
-        __syncthreads();  // every warp is done with this item's spectra, Cc and row spills
-        const int after = (int)s_claim;
-        if (next < n_items) load_cc(next);  // lands while the floor is computed
-        unsigned long long kb = red_k[0];
-        for (int i = 1; i < W; ++i) kb = max(kb, red_k[i]);
-        best = __uint_as_float((unsigned)(kb >> 32));
-        const int peak = (int)(0xffffffffu - (unsigned)kb);
-        // exclusion floor (acquisition.py:155-159)
-        float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + (a.pair0 + lp) % a.B) * a.P : nullptr;
-        float fl = -1.f;
-        if (kRegs && !pm) {
-            // Only the cells within `radius` of the peak are excluded: lags D q + rho0 for q in
-            // [ceil((peak - r - rho0)/D), floor((peak + r - rho0)/D)] (mod 1023), at most 2r/D + 1
-            // of them. Cell q lives at (q1, q2) = (16 q mod 31, 16 q mod 33) (inverse of cell_q).
-            // A lane with none of them takes its plain max.
+            const int peak = bidx == 0x7fffffff ? 0 : bidx;  // all-NaN powers (non-finite input, flagged by K1)
+            // exclusion floor (acquisition.py:155-159) from the scratch rows
+            float fl = -1.f;
+#ifdef GACQ_ABL_NOFLOOR
+            if (false) {
+#else
             if (2 * a.radius + 1 < a.P) {
-                // offset by D * 1023 (> radius + rho0) so both bounds divide as unsigned
-                const unsigned off = (unsigned)(a.D * kChips), D = (unsigned)a.D;
-                const unsigned lo = (unsigned)(peak - a.radius - rho0) + off, hi = (unsigned)(peak + a.radius - rho0) + off;
-                const int qa = (int)__umulhi(lo + D - 1u, a.dmagic) - kChips, qb = (int)__umulhi(hi, a.dmagic) - kChips;
-                unsigned m31 = 0u, mx = 0u;
-                for (int q = qa; q <= qb; ++q) {
-                    const int qq = q < 0 ? q + kChips : q >= kChips ? q - kChips : q;
-                    const int q1 = (16 * qq) % 31, q2 = (16 * qq) % 33;
-                    if (q2 == lane) m31 |= 1u << q1;
-                    if (q2 == 32) {
-                        if (lane == 16 && q1 == 0) mx |= 1u;
-                        if (x1 && q1 == lane) mx |= 1u;
-                        if (x1 && q1 == 31 - lane) mx |= 2u;
+#endif
+#pragma unroll 1
+                for (int rho = 0; rho < D; ++rho) {
+                    // excluded cells of phase rho: lags D q + rho for q in
+                    // [ceil((peak - r - rho)/D), floor((peak + r - rho)/D)] (mod 1023), offset by
+                    // D * 1023 (> r + rho) so both bounds divide as unsigned
+                    const unsigned off = (unsigned)(D * kChips), uD = (unsigned)D;
+                    const unsigned lo = (unsigned)(peak - a.radius - rho) + off, hi = (unsigned)(peak + a.radius - rho) + off;
+                    const int qa = (int)__umulhi(lo + uD - 1u, a.dmagic) - kChips, qb = (int)__umulhi(hi, a.dmagic) - kChips;
+                    unsigned m31 = 0u, mx = 0u;
+                    for (int q = qa; q <= qb; ++q) {
+                        const int qq = q < 0 ? q + kChips : q >= kChips ? q - kChips : q;
+                        const int q1 = (16 * qq) % 31, q2 = (16 * qq) % 33;
+                        if (q2 == lane) m31 |= 1u << q1;
+                        if (q2 == 32) {
+                            if (lane == 16 && q1 == 0) mx |= 1u;
+                            if (x1 && q1 == lane) mx |= 1u;
+                            if (x1 && q1 == 31 - lane) mx |= 2u;
+                        }
                     }
-                }
-                if ((m31 | mx) == 0u) {
-                    fl = lane_max;  // the fake 0 of lanes without coop cells never raises the floor
-                } else {
+                    const float* row = rows + rho * kPhaseRow + lane;
 #pragma unroll
                     for (int q1 = 0; q1 < 31; ++q1)
-                        if (!((m31 >> q1) & 1u)) fl = fmaxf(fl, acc[q1]);
-                    if (x0 && !(mx & 1u)) fl = fmaxf(fl, accx[0]);
-                    if (x1 && !(mx & 2u)) fl = fmaxf(fl, accx[1]);
+                        if (!((m31 >> q1) & 1u)) fl = fmaxf(fl, row[q1 * 32]);
+                    // fake 0 of lanes without coop cells: never raises the floor above a real power
+                    if (!(mx & 1u)) fl = fmaxf(fl, row[31 * 32]);
+                    if (!(mx & 2u)) fl = fmaxf(fl, row[32 * 32]);
                 }
             }
-        } else if (kRegs) {
-            for_cells([&](float v, int lag) {
-                if (!excluded(lag, peak, a.P, a.radius)) fl = fmaxf(fl, v);
-                if (pm) pm[lag] = v;
-            });
-        } else {
-            for (int i = threadIdx.x; i < a.D * kChips; i += blockDim.x) {
-                const int rho = i / kChips, r = i - rho * kChips, q1 = r / 33, q2 = r - q1 * 33;
-                const int lag = a.D * cell_q(q1, q2) + rho;
-                const float v = rows[i];
-                if (!excluded(lag, peak, a.P, a.radius)) fl = fmaxf(fl, v);
-                if (pm) pm[lag] = v;
-            }
-        }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
-        if (lane == 0) red_f[w] = fl;
-        cp_async_wait_all();
-        __syncthreads();  // publishes red_f and the next item's Cc
-        if (threadIdx.x == 0) {
-            float f = red_f[0];
-            for (int i = 1; i < W; ++i) f = fmaxf(f, red_f[i]);
-            const int64_t pair = a.pair0 + lp;
-            const int64_t s = pair / a.B;
-            const int b = (int)(pair - s * a.B);
-            gacq_row out;
-            out.bin = b;
-            out.lag = peak;
-            out.peak = best;
-            out.floor = f < 0.f ? 0.f : f;
-            a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
+            for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
+            if (lane == 0) {
+                const int64_t s = pair / a.B;
+                gacq_row out;
+                out.bin = b;
+                out.lag = peak;
+                out.peak = best;
+                out.floor = fl < 0.f ? 0.f : fl;
+                a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
+            }
+        } else if (znext) {  // idle in this unit: start the next item's first spectrum now
+            __syncwarp();
+            if (lane == 0) bulk_load_nofence(zbuf, znext, kSpecBytes, mbar);
         }
-        item = next;
-        next = after;
-        if (item >= n_items) break;
+        cp_async_wait_all();
+        __syncthreads();  // the next unit's code spectrum and claim are visible; this unit's slot is free
+        unit = nxt;
+        if (unit >= a.n_units) break;
     }
 }
 

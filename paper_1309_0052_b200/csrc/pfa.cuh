@@ -141,26 +141,40 @@ __device__ __forceinline__ void dft33(cx (&x)[33], Emit&& emit) {
     for (int c = 0; c < 3; ++c) dft_odd<S, 11, 5>(y[c], [&](int e, cx v) { emit((22 * c + 12 * e) % 33, v); });
 }
 
-// dft33 with streamed inputs (see dft31_stream): the 3-point layer takes its triples
-// (3b, 11+3b, 22+3b) mod 33 in order b = 0..10, the next triple's loads depending on the
-// previous layer output, so the 11-point layer starts with only y[3][11] live.
-template <int S, typename Load, typename Emit>
-__device__ __forceinline__ void dft33_stream(Load&& load, int zero, Emit&& emit) {
+// dft33 with its inputs loaded through load(k, dep): GACQ_DFT33_AHEAD triples are requested before
+// the 3-point layer starts (11 = all 33 at once, measured fastest: the shared-memory latency is
+// paid once per transform), later triples' addresses depend on the previous layer output (`dep`,
+// a runtime 0) so the compiler keeps the requested window. consumed() runs once every input has
+// been used (after the 3-point layer), then the 11-point layers emit the outputs.
+template <int S, typename Load, typename Consumed, typename Emit>
+__device__ __forceinline__ void dft33_stream(Load&& load, int zero, Consumed&& consumed, Emit&& emit) {
+#ifndef GACQ_DFT33_AHEAD
+#define GACQ_DFT33_AHEAD 11
+#endif
+    constexpr int AH = GACQ_DFT33_AHEAD;
     cx y[3][11];
-    cx n0 = load(0, 0), n1 = load(11, 0), n2 = load(22, 0);
+    cx n[AH][3];
+#pragma unroll
+    for (int a = 0; a < AH; ++a) {
+        n[a][0] = load((3 * a) % 33, 0);
+        n[a][1] = load((11 + 3 * a) % 33, 0);
+        n[a][2] = load((22 + 3 * a) % 33, 0);
+    }
 #pragma unroll
     for (int b = 0; b < 11; ++b) {
-        cx t[3] = {n0, n1, n2};
-        if (b < 10) {
+        cx t[3] = {n[b % AH][0], n[b % AH][1], n[b % AH][2]};
+        if (b + AH < 11) {
+            const int bn = b + AH;
             const int dep = b == 0 ? 0 : (int)(y[2][b - 1] >> 32) & zero;
-            n0 = load((3 * b + 3) % 33, dep);
-            n1 = load((14 + 3 * b) % 33, dep);
-            n2 = load((25 + 3 * b) % 33, dep);
+            n[b % AH][0] = load((3 * bn) % 33, dep);
+            n[b % AH][1] = load((11 + 3 * bn) % 33, dep);
+            n[b % AH][2] = load((22 + 3 * bn) % 33, dep);
         }
         dft3_fma<S>(t);
 #pragma unroll
         for (int c = 0; c < 3; ++c) y[c][b] = t[c];
     }
+    consumed();
 #pragma unroll
     for (int c = 0; c < 3; ++c) dft_odd<S, 11, 5>(y[c], [&](int e, cx v) { emit((22 * c + 12 * e) % 33, v); });
 }
@@ -189,9 +203,20 @@ __device__ __forceinline__ void coop31(cx x, int lane, Coef&& coef, cx* scr, Emi
     }
     __syncwarp();
     const int off = lane >= 17 ? 17 : 0;
-    cx acc = lane >= 17 ? czero() : scr[0];
+#ifndef GACQ_COOP_CHAINS
+#define GACQ_COOP_CHAINS 1
+#endif
+    // GACQ_COOP_CHAINS independent accumulation chains (shorter dependent FFMA2 chains)
+    constexpr int NC = GACQ_COOP_CHAINS;
+    cx part[NC];
+    part[0] = lane >= 17 ? czero() : scr[0];
 #pragma unroll
-    for (int j = 1; j <= 15; ++j) acc = fma2(scr[off + j], bc(coef(j)), acc);
+    for (int c = 1; c < NC; ++c) part[c] = czero();
+#pragma unroll
+    for (int j = 1; j <= 15; ++j) part[(j - 1) % NC] = fma2(scr[off + j], bc(coef(j)), part[(j - 1) % NC]);
+#pragma unroll
+    for (int c = 1; c < NC; ++c) part[0] = add2(part[0], part[c]);
+    const cx acc = part[0];
     const cx bk = __shfl_sync(0xffffffffu, acc, (lane + 16) & 31);
     if (lane >= 1 && lane <= 15) {
         const cx r = rot<S>(bk);
