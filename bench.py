@@ -668,7 +668,7 @@ def measure_gpu_extras(args, be, eng, c, shard, full, rank, world, dist, maxr, b
         for cn in ("c1", "c3"):
             x = be.host(be.batch(CONFIGS[cn], 1, seed=5))[0]
             ms = measure_latency(cn, x) * 1e3
-            entry = {"acquire_all_ms": ms, "cells": 32 * n_bins_of(cc)}
+            entry = {"acquire_all_ms": ms, "cells": 32 * n_bins_of(CONFIGS[cn])}
             if not args.no_cpu_baseline:
                 ctx = mp.get_context("spawn")
                 with ctx.Pool(1, initializer=_cpu_worker_init) as pool:

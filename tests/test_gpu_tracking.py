@@ -1,9 +1,9 @@
 """GPU tracking against the reference's tracking goldens.
 
-Replicas are bit-identical to the reference; the E/P/L sums accumulate in float64 on the
-device (the reference sums left to right in complex64), so correlators are compared within
-TRK_RTOL of the largest correlator magnitude of the epoch, discriminators / NCO states
-within small absolute tolerances, and lock decisions exactly.
+Replicas are bit-identical to the reference and the E/P/L sums are the reference's own
+left-to-right complex64 sums (same float32 addition order), so correlators, discriminators,
+NCO states and lock decisions are compared bit for bit, every epoch. A second test keeps
+tolerance checks (TRK_RTOL of the epoch's largest correlator) as a readable diagnostic.
 """
 
 import numpy as np
