@@ -30,6 +30,7 @@ constexpr int kXch = 1023 + 33;                  // K2 exchange [q2][31] + coop3
 constexpr int kCcHalf = 17 * 31 + 1;             // Hermitian half [k2 <= 16][31] of a conj code spectrum (+ pad)
 constexpr int kCorrWarps = 4;                    // K2 warps per CTA (one item each)
 constexpr int kPhaseRow = 33 * 32;               // K2 scratch row of one phase: [q1 or coop slot][lane] floats
+constexpr int kTop2Row = 5 * 32;                 // K2 (kTop2) phase summary: [max, 2nd max, max index, coop 0, coop 1][lane]
 #ifndef GACQ_PFA_MAXNREG
 #define GACQ_PFA_MAXNREG 168                     // 3 CTAs x 4 warps per SM; no spills (streamed stages)
 #endif
@@ -315,6 +316,12 @@ __device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
 // `radius` of the peak are excluded, and every lane owns at most one q per window (its q values
 // are congruent mod 33), found directly by the inverse map (q1, q2) = (16 q mod 31, 16 q mod 33).
 // acquisition.py:151-159.
+// kTop2 (every window of the exclusion radius holds at most 33 consecutive chip lags, 2 r < 33 D:
+// the default one-chip radius and any r < 16.5 chips): each lane owns at most one excluded cell of
+// its 31 per phase (its q values are congruent mod 33) and at most one of the spread row's, so a
+// phase keeps only the lane's (max, its first index, second max) and the two spread-row cells: 5
+// words per lane instead of the 33-float row, and the floor reads them back with no window loop.
+template <bool kTop2>
 __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
     __shared__ int s_unit[2];
     extern __shared__ __align__(16) cx smem[];
@@ -412,11 +419,35 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                     __syncwarp();  // E is free for the next transform
                 }
                 // phase done: the row to scratch (and the parity power map), the running first argmax
-                float* row = rows + rho * kPhaseRow + lane;
+                float m;
+                if constexpr (kTop2) {
+                    float v1 = -1.f, v2 = -1.f;
+                    int i1 = 0;
 #pragma unroll
-                for (int q1 = 0; q1 < 31; ++q1) row[q1 * 32] = acc[q1];
-                row[31 * 32] = accx[0];
-                row[32 * 32] = accx[1];
+                    for (int q1 = 0; q1 < 31; ++q1) {  // first max, and the second max (ties count twice)
+                        const float v = acc[q1];
+                        const bool gt = v > v1;
+                        v2 = gt ? v1 : fmaxf(v2, v);
+                        i1 = gt ? q1 : i1;
+                        v1 = gt ? v : v1;
+                    }
+                    float* row = rows + rho * kTop2Row + lane;
+                    row[0] = v1;
+                    row[32] = v2;
+                    row[64] = __int_as_float(i1);
+                    row[96] = accx[0];
+                    row[128] = accx[1];
+                    m = v1;
+                } else {
+                    float* row = rows + rho * kPhaseRow + lane;
+#pragma unroll
+                    for (int q1 = 0; q1 < 31; ++q1) row[q1 * 32] = acc[q1];
+                    row[31 * 32] = accx[0];
+                    row[32 * 32] = accx[1];
+                    m = acc[0];
+#pragma unroll
+                    for (int q1 = 1; q1 < 31; ++q1) m = fmaxf(m, acc[q1]);
+                }
                 if (pm) {
 #pragma unroll
                     for (int q1 = 0; q1 < 31; ++q1) pm[D * cell_q(q1, lane) + rho] = acc[q1];
@@ -425,9 +456,6 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 }
                 // lane max (lanes without coop cells keep accx = 0, <= every power, never a lag
                 // candidate), then the lowest lag holding it, searched only when it can win
-                float m = acc[0];
-#pragma unroll
-                for (int q1 = 1; q1 < 31; ++q1) m = fmaxf(m, acc[q1]);
                 m = fmaxf(m, fmaxf(accx[0], accx[1]));
                 if (m >= best) {
                     int bl = 0x7fffffff;
@@ -462,6 +490,27 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
 #else
             if (2 * a.radius + 1 < a.P) {
 #endif
+                if constexpr (kTop2) {
+                    const int cl = (31 * lane) % 33;  // the residue mod 33 of this lane's q values
+#pragma unroll 4
+                    for (int rho = 0; rho < D; ++rho) {
+                        const unsigned off = (unsigned)(D * kChips), uD = (unsigned)D;
+                        const unsigned lo = (unsigned)(peak - a.radius - rho) + off, hi = (unsigned)(peak + a.radius - rho) + off;
+                        const int qa = (int)__umulhi(lo + uD - 1u, a.dmagic) - kChips, qb = (int)__umulhi(hi, a.dmagic) - kChips;
+                        const float* row = rows + rho * kTop2Row + lane;
+                        const float v1 = row[0], v2 = row[32], c0 = row[96], c1 = row[128];
+                        const int i1 = __float_as_int(row[64]);
+                        // the window's one lag of residue cl (this lane's cells) and of residue 2 (row 32)
+                        const int qm = qa + ((cl - qa) % 33 + 33) % 33, qc = qa + ((2 - qa) % 33 + 33) % 33;
+                        const auto wrap = [](int q) { return q < 0 ? q + kChips : q >= kChips ? q - kChips : q; };
+                        const int q1m = qm <= qb ? (16 * wrap(qm)) % 31 : -1;
+                        const int q1c = qc <= qb ? (16 * wrap(qc)) % 31 : -1;
+                        fl = fmaxf(fl, q1m == i1 ? v2 : v1);
+                        // lanes without spread-row cells hold 0 there: never above a real power
+                        if (!(q1c >= 0 && x0 && q1c == (lane == 16 ? 0 : lane))) fl = fmaxf(fl, c0);
+                        if (!(q1c >= 0 && x1 && q1c == 31 - lane)) fl = fmaxf(fl, c1);
+                    }
+                } else {
 #pragma unroll 1
                 for (int rho = 0; rho < D; ++rho) {
                     // excluded cells of phase rho: lags D q + rho for q in
@@ -488,6 +537,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                     // fake 0 of lanes without coop cells: never raises the floor above a real power
                     if (!(mx & 1u)) fl = fmaxf(fl, row[31 * 32]);
                     if (!(mx & 2u)) fl = fmaxf(fl, row[32 * 32]);
+                }
                 }
             }
 #pragma unroll

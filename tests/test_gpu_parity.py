@@ -354,3 +354,31 @@ def test_concurrent_host_threads_on_one_plan(pkg):
     assert not errs, errs[0]
     for i in range(32):
         np.testing.assert_array_equal(got[i], want[i % 8])
+
+
+# exclusion radii around the K2 floor's two forms (gacq_pfa.cuh): phase summaries while
+# 2 r < 33 D (every window holds <= 33 chip lags), the full per-phase rows beyond; the
+# boundary pair at each D, the default one chip, and windows wider than the whole code
+RADIUS_CASES = [(4.092e6, r) for r in (1, 4, 10, 64, 65, 66, 67, 200, 2000, 2045, 2046)] + \
+               [(8.184e6, r) for r in (8, 131, 132, 500)] + [(16.368e6, r) for r in (16, 263, 264)]
+
+
+@pytest.mark.parametrize("fs,radius", RADIUS_CASES)
+def test_exclusion_radius_floor_forms(pkg, fs, radius):
+    kw = dict(doppler_min_hz=-2000.0, doppler_max_hz=2000.0, doppler_step_hz=500.0, noncoherent_rounds=2,
+              exclusion_radius_samples=radius)
+    ocfg = oracle.OracleConfig(**kw)
+    bins = ocfg.doppler_bins_hz()
+    for snap in range(2):
+        x, _ = oracle.make_snapshot(snap, fs, 2e-3, base_seed=8080 + radius)
+        eng = pkg.get_engine(fs, list(range(1, 33)), pkg.AcqConfig(**kw))
+        got = eng.search(x).results()[0]
+        ref = oracle.acquire_all(x, fs, range(1, 33), ocfg)
+        for g, r in zip(got, ref):
+            gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples, peak_metric=g.peak_metric,
+                      detected=g.detected)
+            v = compare(gd, r, kw.get("detection_threshold", 2.5))
+            if v != "exact":
+                pm = oracle.acquire_channel(x, fs, r["prn"], ocfg, want_map=True)["power_map"]
+                v = compare(gd, r, 2.5, pm, bins)
+            assert v == "exact", (fs, radius, snap, r["prn"], v)
