@@ -55,7 +55,7 @@ __device__ __forceinline__ void dft_odd(cx (&x)[P], Emit&& emit) {
             const int k = k0 + kk;
             if (k > H) continue;
             A[kk] = fma2(x[1], bc(tcos<P>(k % P)), x[0]);
-            B[kk] = mul2(x[P - 1], bc(tsin<P>(k % P)));
+            B[kk] = x[P - 1];  // B_k / sin(2 pi k/P): b_1's coefficient is 1
         }
 #pragma unroll
         for (int j = 2; j <= H; ++j)
@@ -64,15 +64,16 @@ __device__ __forceinline__ void dft_odd(cx (&x)[P], Emit&& emit) {
                 const int k = k0 + kk;
                 if (k > H) continue;
                 A[kk] = fma2(x[j], bc(tcos<P>((j * k) % P)), A[kk]);
-                B[kk] = fma2(x[P - j], bc(tsin<P>((j * k) % P)), B[kk]);
+                B[kk] = fma2(x[P - j], bc(tsin<P>((j * k) % P) / tsin<P>(k % P)), B[kk]);
             }
 #pragma unroll
         for (int kk = 0; kk < KB; ++kk) {
             const int k = k0 + kk;
             if (k > H) continue;
+            // X_k, X_(P-k) = A_k +- S i sin(2 pi k/P) B'_k: the sine folds into the output FFMA2s
             const cx r = rot<S>(B[kk]);
-            emit(k, add2(A[kk], r));
-            emit(P - k, sub2(A[kk], r));
+            emit(k, fma2(r, bc(tsin<P>(k % P)), A[kk]));
+            emit(P - k, fma2(r, bc(-tsin<P>(k % P)), A[kk]));
         }
     }
 }

@@ -1,5 +1,5 @@
-# A/B of libgacq builds under exp/: bench C3 K1/K2 times per variant
+# A/B of K2 variants (exp/libgacq_<v>.so) against the in-tree build: tools/gpu_ab.sh "<configs>" v1 v2 ...
 mkdir -p gpurun_out
-for v in "$@"; do
-  GACQ_LIB=exp/libgacq_$v.so timeout 300 python bench.py --steps 10 --no-cpu-baseline --tracking-epochs 1 > gpurun_out/ab_$v.json 2>&1
-done
+CF=$1; shift
+(for cf in $CF; do echo "== $cf"; timeout 900 python tools/k2_ab.py --config $cf --batch $([ $cf = c4 ] && echo 16 || echo 512) default "$@" 2>&1 | cut -c1-330; done) > gpurun_out/ab.log
+cat gpurun_out/ab.log
