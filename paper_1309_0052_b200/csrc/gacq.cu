@@ -249,7 +249,10 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
     const int64_t n_pairs = n_snap * c->B;
     const int64_t n_rows = n_snap * c->n_prn;
     const bool quantized = inp.fmt != kFmtComplex64;
-    const bool staged = !inp.on_device || quantized;
+    // the prime-factor K1 dequantizes integer I/Q in its wipe load; the generic path reads a
+    // complex64 staging copy made by the dequant kernel on the copy stream
+    const bool fused_q = quantized && !c->gen;
+    const bool staged = !inp.on_device || (quantized && !fused_q);
     int rc;
     if ((rc = grow(&c->d_rows_bin, &c->rows_bin_cap, n_rows * c->B))) return rc;
     if (!per_bin && (rc = grow(&c->d_rows, &c->rows_cap, n_rows))) return rc;
@@ -262,16 +265,16 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
     }
     // K1 lowers d_bad to the index of any snapshot holding a NaN or an infinity
     CUDA_TRY(cudaMemsetAsync(c->d_bad, 0x7f, sizeof(int), c->stream));
-    const float2* in = (const float2*)inp.ptr;
+    const void* in = inp.ptr;
     int64_t in_stride = inp.stride;
     // Staging in snapshot chunks on the copy stream (H2D and/or dequantization);
     // chunk k is covered by copy_events[k]
     int64_t copy_chunk = 0, n_copy_chunks = 0;
     if (staged) {
-        if ((rc = grow(&c->d_in, &c->in_cap, n_snap * span))) return rc;
+        if (!fused_q && (rc = grow(&c->d_in, &c->in_cap, n_snap * span))) return rc;
         const int64_t sb = sample_bytes(inp.fmt);
         if (quantized && !inp.on_device && (rc = grow(&c->d_raw, &c->raw_cap, n_snap * span * sb))) return rc;
-        in = c->d_in;
+        in = fused_q ? (const void*)c->d_raw : (const void*)c->d_in;
         in_stride = span;
         // fine-grained copies (<= 16 snapshots per event) so the first compute chunk, which is
         // kept small below, starts after a few MB of H2D rather than after a whole chunk
@@ -291,8 +294,10 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             } else if (!inp.on_device) {
                 CUDA_TRY(cudaMemcpy2DAsync(c->d_raw + s0 * span * sb, span * sb, src + s0 * inp.stride * sb,
                                            inp.stride * sb, span * sb, ns, cudaMemcpyHostToDevice, c->copy_stream));
-                CUDA_TRY(launch_dequant(c, inp, s0, ns, c->d_raw + s0 * span * sb, span, c->d_in + s0 * span, span));
-                c->stats.launches++;
+                if (!fused_q) {
+                    CUDA_TRY(launch_dequant(c, inp, s0, ns, c->d_raw + s0 * span * sb, span, c->d_in + s0 * span, span));
+                    c->stats.launches++;
+                }
             } else {
                 CUDA_TRY(launch_dequant(c, inp, s0, ns, src + s0 * inp.stride * sb, inp.stride, c->d_in + s0 * span,
                                         span));
@@ -324,7 +329,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         }
         cx* Zp = reinterpret_cast<cx*>(c->d_Z);
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
-        GenArgs ga{in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
+        GenArgs ga{(const float2*)in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
                    pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
         const int gen_l = c->logM > kGenMaxLogM ? 2 : 1;
         const int gen_pts = (1 << c->logM) / gen_l;
@@ -339,7 +344,9 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
                 gacq_gen_fwd_kernel<1, 32><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
         } else {
-            FwdPfaArgs fa{in, in_stride, c->d_carrier, Zp, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->K};
+            const int fmt = fused_q ? inp.fmt : kFmtComplex64;
+            const double qs = inp.scale / (inp.fmt == GACQ_FMT_INT8 ? 127.0 : 32767.0);
+            FwdPfaArgs fa{in, in_stride, fmt, qs, c->d_carrier, Zp, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->K};
             CUDA_TRY(launch_fwd_pfa(c, fa, np * c->R));
         }
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); ev++; }

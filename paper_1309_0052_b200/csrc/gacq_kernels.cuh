@@ -34,13 +34,56 @@ __device__ __forceinline__ unsigned fin_word(ulonglong2 v, unsigned fin) { retur
 // both the wipe stores (consecutive n) and the chip-sum loads (consecutive m) conflict-free.
 __host__ __device__ constexpr int fwd_ws(int D) { return kRow + (D <= 16 ? 16 / D : 0); }
 
+// Sample sources of the wipe: complex64, or integer I/Q dequantized in registers exactly as
+// read_if_file does (iffile.py:95-98): float32(float64(q) * s), s = scale / limit from the host.
+// ld2(i, a, b) returns samples 2i and 2i+1 of the block (one load), ld1(n) sample n.
+struct SrcC64 {
+    const cx* x;
+    __device__ __forceinline__ void ld2(int64_t i, cx& a, cx& b) const {
+        const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(x) + i);
+        a = v.x;
+        b = v.y;
+    }
+    __device__ __forceinline__ cx ld1(int64_t n) const { return __ldg(x + n); }
+    __device__ __forceinline__ SrcC64 at(int64_t n) const { return {x + n}; }
+    __device__ __forceinline__ bool aligned() const { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; }
+};
+__device__ __forceinline__ float deq(int q, double s) { return __double2float_rn(__dmul_rn((double)q, s)); }
+// int8: the 256 possible values come from a per-CTA shared-memory table of the same products
+// (lut[q + 128] = deq(q, s)), so the wipe load does no float64 work
+struct SrcI8 {
+    const signed char* q;  // interleaved I/Q bytes
+    const float* lut;      // shared memory, 256 entries
+    __device__ __forceinline__ float v(int b) const { return lut[b + 128]; }
+    __device__ __forceinline__ void ld2(int64_t i, cx& a, cx& b) const {
+        const int w = __ldg(reinterpret_cast<const int*>(q) + i);
+        a = pk(v((signed char)(w & 0xff)), v((signed char)((w >> 8) & 0xff)));
+        b = pk(v((signed char)((w >> 16) & 0xff)), v(w >> 24));
+    }
+    __device__ __forceinline__ cx ld1(int64_t n) const { return pk(v(__ldg(q + 2 * n)), v(__ldg(q + 2 * n + 1))); }
+    __device__ __forceinline__ SrcI8 at(int64_t n) const { return {q + 2 * n, lut}; }
+    __device__ __forceinline__ bool aligned() const { return (reinterpret_cast<uintptr_t>(q) & 3) == 0; }
+};
+struct SrcI16 {
+    const short* q;
+    double s;
+    __device__ __forceinline__ void ld2(int64_t i, cx& a, cx& b) const {
+        const int2 w = __ldg(reinterpret_cast<const int2*>(q) + i);
+        a = pk(deq((short)(w.x & 0xffff), s), deq(w.x >> 16, s));
+        b = pk(deq((short)(w.y & 0xffff), s), deq(w.y >> 16, s));
+    }
+    __device__ __forceinline__ cx ld1(int64_t n) const { return pk(deq(__ldg(q + 2 * n), s), deq(__ldg(q + 2 * n + 1), s)); }
+    __device__ __forceinline__ SrcI16 at(int64_t n) const { return {q + 2 * n, s}; }
+    __device__ __forceinline__ bool aligned() const { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; }
+};
+
 // Wipe-off (bit-exact, acquisition.py:141) of one coherent block x (K code periods) with the
 // carrier replica c, folded over the K periods into the transposed table
 // wt[k][m] = wbar[D m + k]; wt[k][1023] repeats wt[k][0] (circular chip m+1). Coalesced,
-// two samples per 16-byte load. All NT threads of the CTA take part; ends with a barrier whose
-// result is true when any loaded sample of x is a NaN or an infinity.
-template <int D, int NT>
-__device__ __forceinline__ bool wipe_fold(const cx* __restrict__ x, const cx* __restrict__ c, int P, int K,
+// two samples per load. All NT threads of the CTA take part; ends with a barrier whose
+// result is true when any sample of x (after dequantization) is a NaN or an infinity.
+template <int D, int NT, class Src>
+__device__ __forceinline__ bool wipe_fold(const Src x, const cx* __restrict__ c, int P, int K,
                                           cx* __restrict__ wt) {
     constexpr int WS = fwd_ws(D);
     auto put = [&](int n, cx w) {
@@ -48,25 +91,25 @@ __device__ __forceinline__ bool wipe_fold(const cx* __restrict__ x, const cx* __
         wt[k * WS + m] = w;
         if (m == 0) wt[k * WS + kChips] = w;
     };
-    const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(c)) & 15) == 0 && (P & 1) == 0;
+    const bool vec = x.aligned() && (reinterpret_cast<uintptr_t>(c) & 15) == 0 && (P & 1) == 0;
     unsigned fin = 0x7f800000u;
     if (vec) {
-        const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x);
         const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(c);
         const int np = P / 2;
 #ifndef GACQ_WIPE_U
 #define GACQ_WIPE_U 4
 #endif
-        constexpr int U = GACQ_WIPE_U;  // 16-byte load pairs in flight per thread
+        constexpr int U = GACQ_WIPE_U;  // load pairs in flight per thread
         if (K == 1) {  // one code period per block (coherent_ms = 1): no fold, twice the loads in flight
             constexpr int U1 = 2 * U;
             for (int base = threadIdx.x; base < np; base += U1 * NT) {
-                ulonglong2 xv[U1], cv[U1];
+                cx xa[U1], xb[U1];
+                ulonglong2 cv[U1];
 #pragma unroll
                 for (int u = 0; u < U1; ++u) {
                     const int i = base + u * NT;
                     if (i < np) {
-                        xv[u] = __ldg(x2 + i);
+                        x.ld2(i, xa[u], xb[u]);
                         cv[u] = __ldg(c2 + i);
                     }
                 }
@@ -74,9 +117,9 @@ __device__ __forceinline__ bool wipe_fold(const cx* __restrict__ x, const cx* __
                 for (int u = 0; u < U1; ++u) {
                     const int i = base + u * NT;
                     if (i < np) {
-                        fin = fin_word(xv[u], fin);
-                        put(2 * i, cmul_exact(xv[u].x, cv[u].x));
-                        put(2 * i + 1, cmul_exact(xv[u].y, cv[u].y));
+                        fin = fin_word(xa[u], fin_word(xb[u], fin));
+                        put(2 * i, cmul_exact(xa[u], cv[u].x));
+                        put(2 * i + 1, cmul_exact(xb[u], cv[u].y));
                     }
                 }
             }
@@ -85,19 +128,20 @@ __device__ __forceinline__ bool wipe_fold(const cx* __restrict__ x, const cx* __
         for (int base = threadIdx.x; base < np; base += U * NT) {
             cx w[U][2];
             for (int k = 0; k < K; ++k) {
-                ulonglong2 xv[U], cv[U];
+                cx xa[U], xb[U];
+                ulonglong2 cv[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int i = base + u * NT;
                     if (i < np) {
-                        xv[u] = __ldg(x2 + k * np + i);
+                        x.ld2((int64_t)k * np + i, xa[u], xb[u]);
                         cv[u] = __ldg(c2 + k * np + i);
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    if (base + u * NT < np) fin = fin_word(xv[u], fin);
-                    const cx p0 = cmul_exact(xv[u].x, cv[u].x), p1 = cmul_exact(xv[u].y, cv[u].y);
+                    if (base + u * NT < np) fin = fin_word(xa[u], fin_word(xb[u], fin));
+                    const cx p0 = cmul_exact(xa[u], cv[u].x), p1 = cmul_exact(xb[u], cv[u].y);
                     w[u][0] = k ? add2(w[u][0], p0) : p0;
                     w[u][1] = k ? add2(w[u][1], p1) : p1;
                 }
@@ -113,11 +157,11 @@ __device__ __forceinline__ bool wipe_fold(const cx* __restrict__ x, const cx* __
         }
     } else {
         for (int n = threadIdx.x; n < P; n += NT) {
-            const cx x0 = __ldg(&x[n]);
+            const cx x0 = x.ld1(n);
             fin = fin_word(x0, fin);
             cx acc = cmul_exact(x0, __ldg(&c[n]));
             for (int k = 1; k < K; ++k) {
-                const cx xk = __ldg(&x[k * P + n]);
+                const cx xk = x.ld1((int64_t)k * P + n);
                 fin = fin_word(xk, fin);
                 acc = add2(acc, cmul_exact(xk, __ldg(&c[k * P + n])));
             }

@@ -41,10 +41,12 @@ __host__ __device__ constexpr int corr_pfa_smem() { return kCorrWarps * (kSpec +
 // K1 with one phase per warp (W == D) computes every chip sum before any warp writes its
 // exchange tile, so the exchange tiles alias the wiped-block table (one barrier in between)
 __host__ __device__ constexpr bool fwd_pfa_alias(int D, int W) { return W == D; }
-__host__ __device__ constexpr int fwd_pfa_smem(int D, int W) {
+__host__ __device__ constexpr int fwd_pfa_main(int D, int W) {
     return fwd_pfa_alias(D, W) ? 8 * (D * fwd_ws(D) > W * (kBuf + kScr) ? D * fwd_ws(D) : W * (kBuf + kScr))
                                : 8 * (D * fwd_ws(D) + W * (kBuf + kScr));
 }
+// + the int8 dequantization table (256 floats) behind the main region
+__host__ __device__ constexpr int fwd_pfa_smem(int D, int W) { return fwd_pfa_main(D, W) + 256 * 4; }
 
 // ---- bulk async copy + mbarrier (SASS UBLKCP / SYNCS) ------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -94,8 +96,10 @@ __device__ __forceinline__ float pow_acc(cx v, float acc) { return fmaf(im(v), i
 #define GACQ_FWD_MINB(D, W) ((D) >= 13 ? 1 : 16 / (W) > 0 ? 16 / (W) : 1)
 #endif
 struct FwdPfaArgs {
-    const float2* snaps;   // batch base (device), snapshot s at snaps + s*stride
-    int64_t stride;        // complex samples between snapshots
+    const void* snaps;     // batch base (device), snapshot s at sample s*stride
+    int64_t stride;        // samples between snapshots
+    int fmt;               // kSrcC64 (complex64) or GACQ_FMT_INT8 / GACQ_FMT_INT16 interleaved I/Q
+    double qs;             // integer formats: scale / limit (iffile.py:95-98)
     const float2* carrier; // [B][n_coh] wipe-off replicas
     cx* Z;                 // [pairs][R][D][kSpec] spectra
     int* bad;              // atomicMin'd to the index of a snapshot holding a non-finite sample
@@ -116,10 +120,21 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
     const int64_t pair = a.pair0 + lp;
     const int64_t s = pair / a.B;
     const int b = (int)(pair % a.B);
-    const cx* xs = reinterpret_cast<const cx*>(a.snaps) + s * a.stride + (int64_t)rd * a.n_coh;
+    const int64_t x0 = s * a.stride + (int64_t)rd * a.n_coh;  // first sample of the block
     const cx* cs = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * a.n_coh;
-    // D = 4, K = 1 (C1-C3): chip sums computed in the wipe (wipe_chips4), wt then holds z[rho][m]
-    if (wipe_fold<D, 32 * W>(xs, cs, a.P, a.K, wt) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
+    // integer I/Q is dequantized in the wipe's registers (no complex64 staging copy)
+    bool bad;
+    if (a.fmt == GACQ_FMT_INT8) {
+        float* lut = reinterpret_cast<float*>(reinterpret_cast<char*>(smem) + fwd_pfa_main(D, W));
+        for (int i = threadIdx.x; i < 256; i += 32 * W) lut[i] = deq(i - 128, a.qs);
+        __syncthreads();
+        bad = wipe_fold<D, 32 * W>(SrcI8{static_cast<const signed char*>(a.snaps), lut}.at(x0), cs, a.P, a.K, wt);
+    }
+    else if (a.fmt == GACQ_FMT_INT16)
+        bad = wipe_fold<D, 32 * W>(SrcI16{static_cast<const short*>(a.snaps), a.qs}.at(x0), cs, a.P, a.K, wt);
+    else
+        bad = wipe_fold<D, 32 * W>(SrcC64{static_cast<const cx*>(a.snaps)}.at(x0), cs, a.P, a.K, wt);
+    if (bad && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     // One phase per warp (W = D >= 4: C1-C3 at D = 4, the 8.184 MHz default at D = 8): the chip
     // sums once per chip, in place. Thread t takes chips m = 32 W j + t, reads wt[k][m] and
     // wt[k][m + 1] (row 1023 repeats chip 0), and after a barrier overwrites wt[rho][m] =

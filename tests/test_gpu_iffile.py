@@ -75,3 +75,26 @@ def test_quantized_batch_strided_and_device(pkg):
     assert st["launches"] > 0
     with pytest.raises(pkg.InvalidInputError):
         eng.run_rows_quantized(ints.astype(np.int16), fmt, scale)
+
+
+@pytest.mark.parametrize("name", [n for n in IF_CASES if "float32" not in n])
+def test_quantized_misaligned_device_and_generic_path(pkg, name):
+    # K1 dequantizes in its wipe load: an I/Q buffer whose start is not load-aligned takes the
+    # per-sample path, and the generic (non-prime-factor) plan keeps the staging dequant kernel;
+    # both must give the rows of the host-dequantized samples
+    import torch
+
+    c = case(name)
+    fs, samples, fmt, scale, ints = if_decoded(c)
+    eng = pkg.get_engine(fs, c["prns"], pkg.AcqConfig(**c["config"]))
+    want = eng.run_rows(samples)
+    isz = ints.dtype.itemsize
+    raw = torch.zeros(ints.size * isz + 64, dtype=torch.uint8, device="cuda")
+    off = 2 * isz  # one I/Q pair: aligned to the element, not to the 2-pair load
+    raw[off:off + ints.size * isz] = torch.from_numpy(ints.view(np.uint8).copy()).cuda()
+    view = raw[off:off + ints.size * isz].view(torch.int8 if isz == 1 else torch.int16)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(eng.run_rows_quantized(view, fmt, scale), want)
+    gen = pkg.AcqEngine(fs, c["prns"], pkg.AcqConfig(**c["config"]), force_generic=True)
+    np.testing.assert_array_equal(gen.run_rows_quantized(ints, fmt, scale), gen.run_rows(samples))
+    gen.close()
