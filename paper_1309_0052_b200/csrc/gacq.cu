@@ -204,6 +204,32 @@ cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     return cudaGetLastError();
 }
 
+// generic correlation: clusters of gen_split(logM) CTAs (distributed shared memory, gacq_generic.cuh)
+template <int L>
+cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t blocks) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kGenThreads);
+    cfg.dynamicSmemBytes = gen_smem(c->logM);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = L;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gacq_gen_corr_kernel<L>, ga);
+}
+cudaError_t launch_gen_corr(const gacq_ctx* c, const GenArgs& ga, int64_t blocks) {
+    switch (gen_split(c->logM)) {
+        case 8: return launch_gen_corr_l<8>(c, ga, blocks);
+        case 4: return launch_gen_corr_l<4>(c, ga, blocks);
+        case 2: return launch_gen_corr_l<2>(c, ga, blocks);
+        default: return launch_gen_corr_l<1>(c, ga, blocks);
+    }
+}
+
 cudaEvent_t prof_event(gacq_ctx* c, size_t i) {
     while (c->prof_events.size() <= i) {
         cudaEvent_t e;
@@ -331,17 +357,13 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
         GenArgs ga{(const float2*)in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
                    pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
-        const int gen_l = c->logM > kGenMaxLogM ? 2 : 1;
-        const int gen_pts = (1 << c->logM) / gen_l;
-        const int gen_smem = (int)sizeof(float2) * (GACQ_GEN_STOCKHAM ? gen_pts + gen_pts / 16 : gen_pts);
-        const bool gen_v16 = gen_vpt(c->logM - (gen_l == 2)) == 16;
+        const int gen_l = gen_split(c->logM), gen_sm = gen_smem(c->logM);
         if (c->gen) {
-            if (gen_l == 2)
-                gacq_gen_fwd_kernel<2, 32><<<(unsigned)(np * c->R * 2), kGenThreads, gen_smem, c->stream>>>(ga);
-            else if (gen_v16)
-                gacq_gen_fwd_kernel<1, 16><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
-            else
-                gacq_gen_fwd_kernel<1, 32><<<(unsigned)(np * c->R), kGenThreads, gen_smem, c->stream>>>(ga);
+            const unsigned nb = (unsigned)(np * c->R * gen_l);
+            if (gen_l == 8) gacq_gen_fwd_kernel<8><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
+            else if (gen_l == 4) gacq_gen_fwd_kernel<4><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
+            else if (gen_l == 2) gacq_gen_fwd_kernel<2><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
+            else gacq_gen_fwd_kernel<1><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
             CUDA_TRY(cudaGetLastError());
         } else {
             const int fmt = fused_q ? inp.fmt : kFmtComplex64;
@@ -353,14 +375,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (!c->gen) CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
         if (c->gen) {
-            const int cs = gen_corr_smem(c->logM, c->P);
-            if (gen_l == 2)
-                gacq_gen_corr_kernel<2, 32><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
-            else if (gen_v16)
-                gacq_gen_corr_kernel<1, 16><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
-            else
-                gacq_gen_corr_kernel<1, 32><<<(unsigned)(np * c->n_prn), kGenThreads, cs, c->stream>>>(ga);
-            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(launch_gen_corr(c, ga, np * c->n_prn * gen_l));
         } else {
             const int64_t n_units = (np + kCorrWarps - 1) / kCorrWarps * c->n_prn;
             if (n_units + c->corr_slots >= INT32_MAX) return fail(GACQ_ERR_UNSUPPORTED, "chunk too large");
@@ -499,17 +514,18 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     int logM = 0;
     if (gen) {
         // n_coh a power of two: the reference's n_coh-point circular correlation is the M = n_coh
-        // transform itself (no extension), when the correlation kernel's lag capacity
-        // (L kGenMaxM / 2) holds P; otherwise the linear form with M >= n_coh + P - 1
+        // transform itself (no extension); otherwise the linear form with M >= n_coh + P - 1
         while ((int64_t(1) << logM) < n_coh) ++logM;
-        const int64_t lag_cap = (int64_t)(logM > kGenMaxLogM ? 2 : 1) * kGenMaxM / 2;
-        if ((int64_t(1) << logM) != n_coh || P > lag_cap)
+        if ((int64_t(1) << logM) != n_coh)
             while ((int64_t(1) << logM) < n_coh + P - 1) ++logM;
+        logM = std::max(logM, 4);
         if (logM > kGenMaxLogMTotal)
             return fail(GACQ_ERR_UNSUPPORTED,
                         "fs=%.17g Hz, coherent_ms=%d: the generic path's transform (%lld points >= n_coh + P - 1) "
-                        "exceeds %d; chip-aligned rates (fs = D*1.023 MHz) have no limit",
-                        fs, p->coherent_ms, (long long)(int64_t(1) << logM), 2 * kGenMaxM);
+                        "exceeds %d (clusters of %d CTAs x %d points); chip-aligned rates (fs = D*1.023 MHz, "
+                        "D <= 16) take the prime-factor path",
+                        fs, p->coherent_ms, (long long)(int64_t(1) << logM), kGenMaxL * kGenMaxMs, kGenMaxL,
+                        kGenMaxMs);
     }
     const int D = gen ? 0 : (int)(P / 1023), K = gen ? 0 : (int)(n_coh / P);
     int ndev = 0;
@@ -570,7 +586,7 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
                     std::fill(d.begin(), d.end(), 0.0);
                     for (int64_t n = 0; n < n_coh; ++n) d[n] = (double)chips[idx[n]];
                     fft_f64(d);
-                    const int L = M > kGenMaxM ? 2 : 1, Ms = M / L;  // residue-major (gacq_generic.cuh)
+                    const int L = gen_split(logM), Ms = M / L;  // residue-major (gacq_generic.cuh)
                     for (int k = 0; k < M; ++k) {
                         const auto v = std::conj(d[k]) / (double)M;
                         gcc[(size_t)i * M + (k % L) * Ms + k / L] = make_float2((float)v.real(), (float)v.imag());
@@ -631,14 +647,12 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaMalloc(&c->d_gtw, gtw.size() * sizeof(float2)));
         CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-        const int fwd_max = (kGenMaxM + kGenMaxM / 16) * (int)sizeof(float2);
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_fwd_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
-        const int corr1_max = gen_corr_smem(kGenMaxLogM, kGenMaxM / 2);
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, corr1_max));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, corr1_max));
-        CTX_TRY(cudaFuncSetAttribute(gacq_gen_corr_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, fwd_max));
+        const int sm_max = gen_smem(kGenMaxLogMs);
+        for (const void* k : {(const void*)gacq_gen_fwd_kernel<1>, (const void*)gacq_gen_fwd_kernel<2>,
+                              (const void*)gacq_gen_fwd_kernel<4>, (const void*)gacq_gen_fwd_kernel<8>,
+                              (const void*)gacq_gen_corr_kernel<1>, (const void*)gacq_gen_corr_kernel<2>,
+                              (const void*)gacq_gen_corr_kernel<4>, (const void*)gacq_gen_corr_kernel<8>})
+            CTX_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max));
     }
     const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * kSpec) *
                                (int64_t)sizeof(float2);

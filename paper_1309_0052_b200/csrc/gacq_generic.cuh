@@ -11,90 +11,54 @@
 //   r = IDFT_M( DFT_M(w_ext) . conj(DFT_M(c)) / M )[0, P)      (no index wrap for tau < P)
 // so no rescale is needed (the reference's ifft carries 1/N, the table carries 1/M).
 // When N is itself a power of two (e.g. 8.192 MHz) the plan takes M = N: the transform is then
-// the reference's circular correlation directly (j < M = N never reaches the extension), as
-// long as P fits the correlation kernel's lag capacity L kGenMaxM / 2.
+// the reference's circular correlation directly (j < M = N never reaches the extension).
 //
 //   K1 gacq_gen_fwd_kernel : per (snapshot, bin, round): bit-exact wipe-off (kernels.py:78-86),
 //                            periodic extension, zero padding, forward M-point FFT -> Z.
 //   K2 gacq_gen_corr_kernel: per (snapshot, bin, PRN): for every round Z . Cg on load, inverse
 //                            FFT, |.|^2 of the first P lags accumulated in registers; first
 //                            argmax and exclusion floor (acquisition.py:151-159).
-// Both transforms are in place in shared memory: bit-reversed load, then radix-4
-// decimation-in-time passes (two radix-2 stages fused, one barrier per pass). A CTA holds at
-// most kGenMaxM points; for M = 2 kGenMaxM (L = 2) the transform is split by one radix-2 step
-// outside shared memory:
-//   forward, CTA l in {0, 1}: X[2k' + l] = DFT_{M/2}( (x[n] + (-1)^l x[n + M/2]) W_M^(-l n) )
-//   inverse, one CTA:         r[tau] = E_0[tau] + W_M^(tau) E_1[tau],  E_l = IDFT_{M/2}(Y[2k' + l])
-// and spectra / code tables are stored residue-major: slot l (M/L) + k' holds frequency L k' + l.
+// Both transforms are Stockham passes in shared memory (below). A CTA transforms at most
+// kGenMaxMs = 8192 points (16 values per thread across a pass's barrier: no spills); larger M is
+// split by one radix-L step over a cluster of L = M / 8192 CTAs (L <= 8, M <= 65536):
+//   forward, CTA l < L:  X[L k' + l] = DFT_Ms( sum_m x[n + m Ms] W_L^(-l m) W_M^(-l n) ),  Ms = M / L
+//   inverse, CTA l:      E_l = IDFT_Ms(Y[L k' + l]), then each CTA takes a contiguous share of the
+//                        lags and combines r[tau] = sum_l W_M^(l tau) E_l[tau mod Ms], reading the
+//                        other CTAs' E_l straight from their shared memory (distributed shared
+//                        memory of the thread-block cluster)
+// and spectra / code tables are stored residue-major: slot l Ms + k' holds frequency L k' + l.
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 
 #include "gacq_kernels.cuh"
 
 namespace gacq {
 
-constexpr int kGenMaxLogM = 14;
-constexpr int kGenMaxM = 1 << kGenMaxLogM;  // points per CTA: 128 KB of complex64 in shared memory
-constexpr int kGenMaxLogMTotal = kGenMaxLogM + 1;  // M <= 2 kGenMaxM (L = 2)
-constexpr int kGenThreads = 512;  // kGenMaxM = 32 * kGenThreads (gen_fft_stockham)
-#ifndef GACQ_GEN_STOCKHAM
-#define GACQ_GEN_STOCKHAM 1  // register-radix Stockham passes (0: in-place radix-4 DIT from bit-reversed input)
-#endif
-// corr kernel dynamic smem: padded transform buffer of M / L points, plus P floats when L = 1
-inline int gen_corr_smem(int logM, int P) {
-    const int L = logM > kGenMaxLogM ? 2 : 1, pts = (1 << logM) / L;
-    return (int)sizeof(float2) * (GACQ_GEN_STOCKHAM ? pts + pts / 16 : pts) + (L == 1 ? 4 * P : 0);
+constexpr int kGenMaxLogMs = 13;
+constexpr int kGenMaxMs = 1 << kGenMaxLogMs;        // points per CTA transform
+constexpr int kGenMaxL = 8;                         // CTAs per cluster (portable cluster size)
+constexpr int kGenMaxLogMTotal = kGenMaxLogMs + 3;  // M <= 65536
+constexpr int kGenThreads = 512;
+constexpr int kGenVPT = kGenMaxMs / kGenThreads;    // values per thread per pass (16)
+constexpr int kGenLags = kGenMaxMs / kGenThreads;   // lags per thread: a CTA's share of P is <= Ms
+__host__ __device__ constexpr int gen_split(int logM) { return logM > kGenMaxLogMs ? 1 << (logM - kGenMaxLogMs) : 1; }
+// the CTA transform's twiddles W_Ms^e, e < Ms/2, copied into shared memory once per CTA: the
+// Stockham passes read them there instead of from global memory (long-scoreboard stalls)
+__host__ __device__ constexpr int gen_tws_bytes(int logM) { return (int)sizeof(float2) * ((1 << logM) / gen_split(logM) / 2); }
+// dynamic smem of both generic kernels: one padded CTA transform (gpad), then (correlation
+// kernel) the power accumulators of the CTA's lags, <= Ms floats: in shared memory rather than
+// registers, where they would stay live across the transform and spill; then the twiddles
+__host__ __device__ constexpr int gen_smem(int logM) {
+    return (int)sizeof(float2) * ((1 << logM) / gen_split(logM) + (1 << logM) / gen_split(logM) / 16) +
+           (int)sizeof(float) * ((1 << logM) / gen_split(logM)) + gen_tws_bytes(logM);
 }
-
-// In-place DFT of x[0, 2^logM) held in bit-reversed order, natural order out.
-// tw[e * tw_stride] = (cos, sin)(2 pi e / 2^logM), e < 2^logM / 2; S = -1 forward, +1 inverse
-// (unnormalised).
-template <int S>
-__device__ __forceinline__ void gen_fft_inplace(cx* __restrict__ x, int logM, const float2* __restrict__ tw,
-                                                int tw_stride) {
-    const int M = 1 << logM;
-    auto wtab = [&](int e) {
-        const float2 t = __ldg(&tw[e * tw_stride]);
-        return pk(t.x, S < 0 ? -t.y : t.y);
-    };
-    int s = 0;
-    if (logM & 1) {  // one radix-2 stage of half-size 1
-        for (int i = threadIdx.x; i < M / 2; i += blockDim.x) {
-            const cx a = x[2 * i], b = x[2 * i + 1];
-            x[2 * i] = add2(a, b);
-            x[2 * i + 1] = sub2(a, b);
-        }
-        __syncthreads();
-        s = 1;
-    }
-    for (; s < logM; s += 2) {
-        // stages s (half-size h) and s+1 (half-size 2h) over blocks of 4h
-        const int h = 1 << s;
-        for (int q = threadIdx.x; q < M / 4; q += blockDim.x) {
-            const int j = q & (h - 1);
-            const int base = ((q >> s) << (s + 2)) + j;
-            cx a0 = x[base], a1 = x[base + h], a2 = x[base + 2 * h], a3 = x[base + 3 * h];
-            const cx w1 = wtab(j << (logM - s - 1));  // W_{2h}^j
-            const cx w2 = wtab(j << (logM - s - 2));  // W_{4h}^j
-            const cx t1 = cmul(a1, w1), t3 = cmul(a3, w1);
-            const cx b0 = add2(a0, t1), b1 = sub2(a0, t1), b2 = add2(a2, t3), b3 = sub2(a2, t3);
-            const cx u2 = cmul(b2, w2), u3 = rot<S>(cmul(b3, w2));  // W_{4h}^{j+h} = W_{4h}^j (S i)
-            x[base] = add2(b0, u2);
-            x[base + 2 * h] = sub2(b0, u2);
-            x[base + h] = add2(b1, u3);
-            x[base + 3 * h] = sub2(b1, u3);
-        }
-        __syncthreads();
-    }
-}
-
-__device__ __forceinline__ int bitrev(int j, int logM) { return (int)(__brev((unsigned)j) >> (32 - logM)); }
 
 // (cos, S sin)(2 pi e / M) for any e in [0, M) from the half table (W^(e + M/2) = -W^e)
 template <int S>
 __device__ __forceinline__ cx gen_tw(const float2* __restrict__ tw, int e, int M) {
     const bool hi = e >= (M >> 1);
-    const float2 t = __ldg(&tw[hi ? e - (M >> 1) : e]);
+    const float2 t = tw[hi ? e - (M >> 1) : e];  // shared-memory table in the passes, global otherwise
     const float c = hi ? -t.x : t.x, sn = hi ? -t.y : t.y;
     return pk(c, S < 0 ? -sn : sn);
 }
@@ -181,18 +145,6 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs,
     __syncthreads();
 }
 
-// In-place natural-order DFT of x[0, 2^logMs) (sign S, unnormalised): radix-16 passes, then
-// one radix-8/4/2 pass for the remaining bits. Needs 2^logMs <= VPT * blockDim; VPT = 16 halves
-// the values each thread holds across a pass's barrier (no spills at 128 registers).
-template <int S, int VPT>
-__device__ __forceinline__ void gen_fft_stockham(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, int L) {
-    int logNs = 0;
-    for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16, VPT>(x, logMs, logNs, tw, L);
-    const int rem = logMs - logNs;
-    if (rem == 3) gen_stockham_pass<S, 8, VPT>(x, logMs, logNs, tw, L);
-    else if (rem == 2) gen_stockham_pass<S, 4, VPT>(x, logMs, logNs, tw, L);
-    else if (rem == 1) gen_stockham_pass<S, 2, VPT>(x, logMs, logNs, tw, L);
-}
 // As gen_fft_stockham, with the first (radix-16, twiddle-free) pass reading load(i) for x[i]:
 // the inputs come straight from global memory, saving one shared-memory round trip and a barrier.
 template <int S, int VPT, class Load>
@@ -206,10 +158,6 @@ __device__ __forceinline__ void gen_fft_stockham_ld(cx* __restrict__ x, int logM
     else if (rem == 2) gen_stockham_pass<S, 4, VPT>(x, logMs, logNs, tw, L);
     else if (rem == 1) gen_stockham_pass<S, 2, VPT>(x, logMs, logNs, tw, L);
 }
-// values per thread of a transform of 2^logMs points on kGenThreads threads
-constexpr int gen_vpt(int logMs) { return (1 << logMs) <= 16 * 512 ? 16 : 32; }
-
-
 
 struct GenArgs {
     const float2* snaps;    // batch base (device), snapshot s at snaps + s*stride
@@ -226,12 +174,12 @@ struct GenArgs {
 };
 
 
-// grid: pairs_in_chunk * R * L CTAs of kGenThreads; dynamic smem (M / L) * 8 bytes;
-// VPT = gen_vpt(logM - (L == 2))
-template <int L, int VPT>
+// grid: pairs_in_chunk * R * L CTAs of kGenThreads (part l = blockIdx.x % L); dynamic smem gen_smem
+template <int L>
 __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a) {
     extern __shared__ __align__(16) cx sm[];
-    const int M = 1 << a.logM, Ms = M / L, logMs = a.logM - (L == 2), N = a.n_coh;
+    const int M = 1 << a.logM, logMs = a.logM - (L == 8 ? 3 : L == 4 ? 2 : L == 2 ? 1 : 0), Ms = 1 << logMs;
+    const int N = a.n_coh;
     const int part = blockIdx.x % L, lr = blockIdx.x / L;
     const int lp = lr / a.R, rd = lr % a.R;
     const int64_t pair = a.pair0 + lp;
@@ -248,105 +196,88 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
         fin = fin_word(xv, fin);
         return cmul_exact(xv, __ldg(&c[n]));  // acquisition.py:141, kernels.py:78-86
     };
-    auto input = [&](int j) {  // transform input j (the L = 2 split folds in its radix-2 step)
+    auto input = [&](int j) {  // transform input j: the radix-L split step folded in
         cx y = wext(j);
-        if (L == 2) {
-            const cx u = wext(j + Ms);
-            y = part == 0 ? add2(y, u) : cmul(sub2(y, u), gen_tw<-1>(a.tw, j, M));
+        if constexpr (L > 1) {
+#pragma unroll
+            for (int m = 1; m < L; ++m) y = add2(y, cmul(wext(j + m * Ms), gen_tw<-1>(a.tw, ((part * m) % L) * Ms, M)));
+            if (part) y = cmul(y, gen_tw<-1>(a.tw, part * j, M));
         }
         return y;
     };
-#if GACQ_GEN_STOCKHAM
-    gen_fft_stockham_ld<-1, VPT>(sm, logMs, a.tw, L, input);  // read straight into the first pass
-#else
-#pragma unroll 4
-    for (int j = threadIdx.x; j < Ms; j += blockDim.x) sm[bitrev(j, logMs)] = input(j);
+    float2* tws = reinterpret_cast<float2*>(reinterpret_cast<float*>(sm + Ms + Ms / 16) + Ms);
+    for (int e = threadIdx.x; e < Ms / 2; e += blockDim.x) tws[e] = __ldg(&a.tw[e * L]);  // W_Ms^e = W_M^(e L)
     __syncthreads();
-    gen_fft_inplace<-1>(sm, logMs, a.tw, L);
-#endif
+    gen_fft_stockham_ld<-1, kGenVPT>(sm, logMs, tws, 1, input);  // read straight into the first pass
     if (__syncthreads_or(fin == 0u) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
-    for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[GACQ_GEN_STOCKHAM ? gpad(k) : k];
+    for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[gpad(k)];
 }
 
-// grid: pairs_in_chunk * n_prn CTAs of kGenThreads (item = lp * n_prn + pi);
-// dynamic smem: the transform buffer (M / L) * 8 bytes (padded), then for L = 1 the P float
-// power accumulators (shared memory rather than registers: live across the transform they
-// would push the 512-thread CTA past its 128 registers -- gen_corr_smem)
-template <int L, int VPT>
+// grid: pairs_in_chunk * n_prn * L CTAs of kGenThreads, clusters of L along x (item =
+// blockIdx.x / L = lp * n_prn + pi, part = cluster rank); dynamic smem gen_smem. CTA `part`
+// owns lags [part Pc, (part + 1) Pc), Pc = ceil(P / L), and their power accumulators.
+template <int L>
 __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a) {
+    namespace cg = cooperative_groups;
     extern __shared__ __align__(16) cx sm[];
     __shared__ float red_v[kGenThreads / 32], red_f[kGenThreads / 32];
     __shared__ int red_i[kGenThreads / 32];
-    constexpr int kPer = L * kGenMaxM / 2 / kGenThreads;  // lags per thread (P <= M/2)
-    const int M = 1 << a.logM, Ms = M / L, logMs = a.logM - (L == 2);
-    const int lp = blockIdx.x / a.n_prn, pi = blockIdx.x % a.n_prn;
-    const cx* cg = a.Cg + (int64_t)pi * M;
-    constexpr bool kSmemAcc = L == 1;
-    float acc[kSmemAcc ? 1 : kPer];
-    float* accs = reinterpret_cast<float*>(sm + (GACQ_GEN_STOCKHAM ? Ms + Ms / 16 : Ms));
-    // power accumulator of this thread's lag i (t = threadIdx.x + i kGenThreads < P)
-    auto A = [&](int i) -> float& { return kSmemAcc ? accs[threadIdx.x + i * kGenThreads] : acc[i]; };
-    cx e0[L == 2 ? kPer : 1];  // E_0 of this thread's lags while E_1 is computed
+    __shared__ float s_best, s_floor;
+    __shared__ int s_bidx;
+    const int M = 1 << a.logM, logMs = a.logM - (L == 8 ? 3 : L == 4 ? 2 : L == 2 ? 1 : 0), Ms = 1 << logMs;
+    const int item = blockIdx.x / L, part = blockIdx.x % L;
+    const int lp = item / a.n_prn, pi = item % a.n_prn;
+    const cx* cgt = a.Cg + (int64_t)pi * M + (int64_t)part * Ms;
+    const int Pc = (a.P + L - 1) / L, t0 = part * Pc, t1 = min(a.P, t0 + Pc);
+    cg::cluster_group cl = cg::this_cluster();
+    float* acc = reinterpret_cast<float*>(sm + Ms + Ms / 16) + threadIdx.x;  // lag t0 + tid + i*512 at acc[i*512]
+    float2* tws = reinterpret_cast<float2*>(reinterpret_cast<float*>(sm + Ms + Ms / 16) + Ms);
+    for (int e = threadIdx.x; e < Ms / 2; e += blockDim.x) tws[e] = __ldg(&a.tw[e * L]);  // W_Ms^e = W_M^(e L)
 #pragma unroll
-    for (int i = 0; i < kPer; ++i)
-        if (!kSmemAcc || threadIdx.x + i * kGenThreads < a.P) A(i) = 0.f;
+    for (int i = 0; i < kGenLags; ++i)
+        if ((int)threadIdx.x + i * kGenThreads < Ms) acc[i * kGenThreads] = 0.f;  // the region holds Ms floats
     for (int rd = 0; rd < a.R; ++rd) {
-        const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M;
+        // an opaque copy of logMs per round: the passes' thread-invariant addresses are then
+        // recomputed each round instead of hoisted out of the loop and held live (spills)
+        int lgs = logMs;
+        asm volatile("" : "+r"(lgs));
+        cx* const X = sm;
+        const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
+        // Z . Cg read straight into the first pass (logMs >= 4 on this path)
+        gen_fft_stockham_ld<1, kGenVPT>(X, lgs, tws, 1, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cgt[k])); });
+        if constexpr (L > 1) cl.sync();  // every E_l complete
+#pragma unroll 2
+        for (int i = 0; i < kGenLags; ++i) {
+            const int t = t0 + threadIdx.x + i * kGenThreads;
+            if (t < t1) {
+                const int e = gpad(t & (Ms - 1));
+                cx v;
+                if constexpr (L == 1) {
+                    v = X[e];
+                } else {  // E_l of every CTA of the cluster (distributed shared memory)
+                    v = *cl.map_shared_rank(X + e, 0);
 #pragma unroll
-        for (int part = 0; part < L; ++part) {
-#if GACQ_GEN_STOCKHAM
-            // Z . Cg read straight into the first pass (logMs >= 4 on this path)
-            gen_fft_stockham_ld<1, VPT>(sm, logMs, a.tw, L, [&](int k) {
-                return cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
-            });
-#else
-#pragma unroll 8  // keep 16 L2 loads in flight per thread
-            for (int k = threadIdx.x; k < Ms; k += blockDim.x)
-                sm[bitrev(k, logMs)] = cmul(__ldg(&z[part * Ms + k]), __ldg(&cg[part * Ms + k]));
-            __syncthreads();
-            gen_fft_inplace<1>(sm, logMs, a.tw, L);
-#endif
-            if constexpr (kSmemAcc) {
-                // lag t = tid + i kGenThreads sits at sb[i kSt] (gpad(tid + 512 i) = gpad(tid) + 544 i):
-                // one base address instead of kPer, which would stay live across the transform
-                constexpr int kSt = GACQ_GEN_STOCKHAM ? kGenThreads + kGenThreads / 16 : kGenThreads;
-                const cx* sb = sm + (GACQ_GEN_STOCKHAM ? gpad(threadIdx.x) : threadIdx.x);
-                float* ab = accs + threadIdx.x;
-                const int nl = (a.P - (int)threadIdx.x + kGenThreads - 1) / kGenThreads;
-#pragma unroll
-                for (int i = 0; i < kPer; ++i) {
-                    if (i < nl) {
-                        const cx v = sb[i * kSt];
-                        ab[i * kGenThreads] = fmaf(im(v), im(v), fmaf(re(v), re(v), ab[i * kGenThreads]));
-                    }
+                    for (int l = 1; l < L; ++l)
+                        v = add2(v, cmul(*cl.map_shared_rank(X + e, l), gen_tw<1>(a.tw, (l * t) & (M - 1), M)));
                 }
-            } else {
-#pragma unroll
-            for (int i = 0; i < kPer; ++i) {
-                const int t = threadIdx.x + i * kGenThreads;
-                if (t < a.P) {
-                    cx v = sm[GACQ_GEN_STOCKHAM ? gpad(t) : t];
-                    if (L == 2 && part == 0) {
-                        e0[i] = v;
-                        continue;
-                    }
-                    if (L == 2) v = add2(e0[i], cmul(v, gen_tw<1>(a.tw, t, M)));  // E_0 + W_M^t E_1
-                    A(i) = fmaf(im(v), im(v), fmaf(re(v), re(v), A(i)));  // acquisition.py:149
-                }
+                float& A = acc[i * kGenThreads];
+                A = fmaf(im(v), im(v), fmaf(re(v), re(v), A));  // acquisition.py:149
             }
-            }
-            __syncthreads();
         }
+        if constexpr (L > 1) cl.sync();  // every CTA has read E_l before the next round overwrites it
+        else __syncthreads();
+        // (measured: alternating two buffers to drop this barrier was no faster, at 2x the smem)
     }
+    // first argmax (value desc, lag asc) over the cluster, then the exclusion floor (acquisition.py:151-159)
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     auto better = [](float v, int l, float bv, int bl) { return v > bv || (v == bv && l < bl); };
     float best = -1.f;
     int bidx = 0x7fffffff;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        const int t = threadIdx.x + i * kGenThreads;
-        if (t < a.P && better(A(i), t, best, bidx)) { best = A(i); bidx = t; }
+    for (int i = 0; i < kGenLags; ++i) {
+        const int t = t0 + threadIdx.x + i * kGenThreads;
+        if (t < t1 && better(acc[i * kGenThreads], t, best, bidx)) { best = acc[i * kGenThreads]; bidx = t; }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -356,10 +287,24 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     }
     if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
     __syncthreads();
-    best = red_v[0];
-    bidx = red_i[0];
-    for (int i = 1; i < nw; ++i)
-        if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
+    if (threadIdx.x == 0) {
+        best = red_v[0];
+        bidx = red_i[0];
+        for (int i = 1; i < nw; ++i)
+            if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
+        s_best = best;
+        s_bidx = bidx;
+    }
+    if constexpr (L > 1) cl.sync(); else __syncthreads();
+    best = s_best;
+    bidx = s_bidx;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        if (l == part) continue;
+        const float ov = *cl.map_shared_rank(&s_best, l);
+        const int oi = *cl.map_shared_rank(&s_bidx, l);
+        if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
+    }
     if (bidx == 0x7fffffff) { best = 0.f; bidx = 0; }  // all-NaN powers (non-finite input, flagged by K1)
     const int64_t pair = a.pair0 + lp;
     const int64_t s = pair / a.B;
@@ -367,13 +312,13 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
     float fl = -1.f;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        const int t = threadIdx.x + i * kGenThreads;
-        if (t < a.P) {
+    for (int i = 0; i < kGenLags; ++i) {
+        const int t = t0 + threadIdx.x + i * kGenThreads;
+        if (t < t1) {
             int d = abs(t - bidx);
             d = min(d, a.P - d);
-            if (d > a.radius) fl = fmaxf(fl, A(i));  // acquisition.py:155-159
-            if (pm) pm[t] = A(i);
+            if (d > a.radius) fl = fmaxf(fl, acc[i * kGenThreads]);  // acquisition.py:155-159
+            if (pm) pm[t] = acc[i * kGenThreads];
         }
     }
 #pragma unroll
@@ -383,6 +328,13 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     if (threadIdx.x == 0) {
         float f = red_f[0];
         for (int i = 1; i < nw; ++i) f = fmaxf(f, red_f[i]);
+        s_floor = f;
+    }
+    if constexpr (L > 1) cl.sync(); else __syncthreads();
+    if (part == 0 && threadIdx.x == 0) {
+        float f = s_floor;
+#pragma unroll
+        for (int l = 1; l < L; ++l) f = fmaxf(f, *cl.map_shared_rank(&s_floor, l));
         gacq_row out;
         out.bin = b;
         out.lag = bidx;
@@ -390,6 +342,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
         out.floor = f < 0.f ? 0.f : f;
         a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
     }
+    if constexpr (L > 1) cl.sync();  // rank 0 has read every CTA's shared memory
 }
 
 }  // namespace gacq

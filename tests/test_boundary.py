@@ -92,14 +92,14 @@ def test_buffer_validation_order_and_messages(pkg):
 
 
 def test_create_rejects_oversized_generic_rate_before_touching_a_device(pkg):
-    # 20 MHz is not chip-aligned and its generic transform (n_coh + P - 1 -> 65536 points)
-    # exceeds the two-CTA limit: refused loudly, never a CPU path
+    # 40 MHz is not chip-aligned and its generic transform (n_coh + P - 1 -> 131072 points)
+    # exceeds the 8-CTA cluster (8 x 8192 points): refused loudly, never a CPU path
     with pytest.raises(pkg.UnsupportedError, match="generic path"):
-        pkg.AcqEngine(20e6, [1], pkg.AcqConfig())
-    # 8.192 MHz with 5 ms coherent: 40960 + 8192 - 1 points -> 65536, also refused (4 ms,
-    # n_coh = 32768, is a power of two and runs as the 32768-point circular transform)
+        pkg.AcqEngine(40e6, [1], pkg.AcqConfig())
+    # 20 MHz with 3 ms coherent: 60000 + 20000 - 1 points -> 131072, also refused (20 MHz at 1
+    # and 2 ms, 65536 points, run on the cluster)
     with pytest.raises(pkg.UnsupportedError, match="generic path"):
-        pkg.AcqEngine(8.192e6, [1], pkg.AcqConfig(coherent_ms=5))
+        pkg.AcqEngine(20e6, [1], pkg.AcqConfig(coherent_ms=3))
 
 
 def test_create_without_gpu_raises_resource_error(pkg):

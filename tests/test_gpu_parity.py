@@ -40,15 +40,10 @@ def run_case(pkg, c):
                  multiplications_performed=r.multiplications_performed) for r in res]
 
 
-# rates the device path does not serve yet (transform > 32768 points, or D > 16): they raise
-# UnsupportedError today; kept in the fixture so the oracle is pinned on them
-PENDING = {"gen20M_snap0", "gen20M_snap1", "gen16367k_coh2", "gen8M192_coh5", "d20_snap0", "d32_snap0"}
-
-
 @pytest.mark.parametrize("name", [c["name"] for c in load_cases()])
 def test_golden_case(pkg, name):
-    if name in PENDING:
-        pytest.skip("large-transform rate not served by the device path yet")
+    # every golden runs, including the 65536-point generic transforms of 20 MHz, 16.367 MHz x
+    # 2 ms, 8.192 MHz x 5 ms and the chip-aligned D = 20 / 32 rates (8-CTA clusters)
     c = case(name)
     got = run_case(pkg, c)
     cfg = oracle_config(c)
@@ -233,7 +228,7 @@ def test_plans_with_different_rates_coexist(pkg):
 
 GENERIC_ON_ALIGNED = ["c1_snap0", "c1_snap1", "c3_snap0", "coh2_snap0", "fs8_snap0", "radius10_snap1",
                       "direct_full_2046k", "zeros_c1", "noise_seed0", "ka_prn5_1500_4000",
-                      "c4_snap0"]  # 16.368 MHz: M = 32768, the two-part (L = 2) transform
+                      "c4_snap0"]  # 16.368 MHz: M = 32768, a 4-CTA cluster transform
 
 
 @pytest.mark.parametrize("name", GENERIC_ON_ALIGNED)
@@ -267,10 +262,10 @@ def test_generic_rates_use_the_generic_path(pkg):
     eng.close()
 
 
-@pytest.mark.parametrize("coherent_ms,fft_len", [(1, 8192), (2, 16384), (4, 32768)])
+@pytest.mark.parametrize("coherent_ms,fft_len", [(1, 8192), (2, 16384), (4, 32768), (8, 65536)])
 def test_power_of_two_rate_runs_the_circular_transform(pkg, coherent_ms, fft_len):
     # 8.192 MHz: n_coh = 8192 * coherent_ms is a power of two, so the reference's n_coh-point
-    # circular correlation is the M = n_coh transform itself (no extension; L = 2 at 32768)
+    # circular correlation is the M = n_coh transform itself (no extension; clusters of M / 8192)
     fs = 8.192e6
     cfg = pkg.AcqConfig(doppler_min_hz=-1000.0, doppler_max_hz=1000.0, doppler_step_hz=250.0,
                         coherent_ms=coherent_ms, noncoherent_rounds=2)
