@@ -86,6 +86,98 @@ void ca_code(int prn, int8_t* out) {
     }
 }
 
+// Generic-path transform plan: M = n_coh when n_coh = 2^a 3^b 5^c (native, circular), else the
+// power of two >= n_coh + P - 1 (linear); L CTAs of Ms = M / L points each (gacq_generic.cuh)
+struct GenPlan {
+    int M = 0, L = 1, Ms = 0, n_pass = 0;
+    bool native = false;
+    signed char radix[gacq::kGenMaxPasses] = {};
+    unsigned long long sched() const {
+        unsigned long long v = 0;
+        for (int p = 0; p < n_pass; ++p) v |= (unsigned long long)gacq::gen_radix_code(radix[p]) << (4 * p);
+        return v;
+    }
+};
+
+bool smooth235(int64_t n) {
+    for (int p : {2, 3, 5})
+        while (n % p == 0) n /= p;
+    return n == 1;
+}
+
+// Stockham radix schedule of an Ms-point CTA transform: radix 16 while it divides, one 8/4/2
+// pass for the remaining power of two, then the fives and threes
+void gen_passes(GenPlan& g) {
+    int m = g.Ms, e2 = 0;
+    while (m % 2 == 0) { m /= 2; ++e2; }
+    g.n_pass = 0;
+    // 2^e2 as radix-16 passes and one 8 or 4; a lone remaining factor 2 becomes (8, 4) in
+    // place of (16, 2) (the radix-2 pass is the most expensive per flop)
+    int n16 = e2 / 4, rem = e2 % 4;
+    if (rem == 1 && n16 > 0) { --n16; rem = 5; }
+    for (int i = 0; i < n16; ++i) g.radix[g.n_pass++] = 16;
+    if (rem == 5) { g.radix[g.n_pass++] = 8; g.radix[g.n_pass++] = 4; }
+    else if (rem) g.radix[g.n_pass++] = (signed char)(1 << rem);
+    for (; m % 5 == 0; m /= 5) g.radix[g.n_pass++] = 5;
+    for (; m % 3 == 0; m /= 3) g.radix[g.n_pass++] = 3;
+}
+
+// false when no transform of at most kGenMaxM points serves (n_coh, P)
+bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
+    if (smooth235(n_coh) && n_coh >= 16) {
+        for (int L = 1; L <= gacq::kGenMaxL; L *= 2) {
+            if (n_coh % L) break;
+            const int64_t Ms = n_coh / L;
+            const bool pow2 = (Ms & (Ms - 1)) == 0;
+            if (Ms <= (pow2 ? gacq::kGenMaxMs : gacq::kGenMaxMsOdd)) {
+                g.native = true;
+                g.M = (int)n_coh;
+                g.L = L;
+                g.Ms = (int)Ms;
+                gen_passes(g);
+                return true;
+            }
+        }
+    }
+    int64_t M = 16;
+    while (M < n_coh + P - 1) M *= 2;
+    if (M > gacq::kGenMaxM) return false;
+    g.native = false;
+    g.M = (int)M;
+    g.L = (int)std::max<int64_t>(1, M / gacq::kGenMaxMs);
+    g.Ms = (int)(M / g.L);
+    gen_passes(g);
+    return true;
+}
+
+// mixed-radix complex DFT in float64, sign -1 (forward), any length (recursive decimation in
+// time over its smallest prime factors; every twiddle from cos/sin of its own angle)
+void dft_f64_rec(std::complex<double>* x, int64_t n) {
+    if (n == 1) return;
+    int64_t p = 2;
+    while (n % p) ++p;
+    const int64_t m = n / p;
+    std::vector<std::complex<double>> sub((size_t)n);
+    for (int64_t r = 0; r < p; ++r)
+        for (int64_t j = 0; j < m; ++j) sub[(size_t)(r * m + j)] = x[j * p + r];
+    for (int64_t r = 0; r < p; ++r) dft_f64_rec(sub.data() + r * m, m);
+    std::vector<std::complex<double>> t((size_t)p);
+    for (int64_t k = 0; k < m; ++k) {
+        for (int64_t r = 0; r < p; ++r) {
+            const double ang = -kTwoPi * (double)(r * k) / (double)n;
+            t[(size_t)r] = sub[(size_t)(r * m + k)] * std::complex<double>(std::cos(ang), std::sin(ang));
+        }
+        for (int64_t q = 0; q < p; ++q) {
+            std::complex<double> acc = 0.0;
+            for (int64_t r = 0; r < p; ++r) {
+                const double ang = -kTwoPi * (double)((r * q) % p) / (double)p;
+                acc += t[(size_t)r] * std::complex<double>(std::cos(ang), std::sin(ang));
+            }
+            x[k + m * q] = acc;
+        }
+    }
+}
+
 // iterative radix-2 complex FFT in float64, sign -1 (forward)
 void fft_f64(std::vector<std::complex<double>>& a) {
     const size_t n = a.size();
@@ -116,7 +208,7 @@ struct gacq_ctx {
     int n_coh = 0, P = 0, D = 0, K = 0, R = 0, B = 0, n_prn = 0, radius = 0;
     float2* d_ccp = nullptr;  // PFA conj code spectra [n_prn][kCcHalf]
     bool gen = false;         // generic power-of-two path (rates that are not chip-aligned)
-    int logM = 0;             // its transform length M = 2^logM >= n_coh + P - 1
+    GenPlan gp;               // its transform (gacq_generic.cuh): M, CTAs per cluster, passes
     float2* d_gtw = nullptr;  // [M/2] (cos, sin)(2 pi e / M)
     float2* d_gcc = nullptr;  // [n_prn][M] conj(DFT_M(code replica)) / M
     std::vector<double> bins;
@@ -204,13 +296,13 @@ cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     return cudaGetLastError();
 }
 
-// generic correlation: clusters of gen_split(logM) CTAs (distributed shared memory, gacq_generic.cuh)
-template <int L>
+// generic correlation: clusters of gp.L CTAs (distributed shared memory, gacq_generic.cuh)
+template <int L, bool kP2>
 cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t blocks) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(kGenThreads);
-    cfg.dynamicSmemBytes = gen_smem(c->logM);
+    cfg.dynamicSmemBytes = gen_smem(c->gp.Ms);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -219,14 +311,19 @@ cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t bloc
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gacq_gen_corr_kernel<L>, ga);
+    return cudaLaunchKernelEx(&cfg, gacq_gen_corr_kernel<L, kP2>, ga);
 }
 cudaError_t launch_gen_corr(const gacq_ctx* c, const GenArgs& ga, int64_t blocks) {
-    switch (gen_split(c->logM)) {
-        case 8: return launch_gen_corr_l<8>(c, ga, blocks);
-        case 4: return launch_gen_corr_l<4>(c, ga, blocks);
-        case 2: return launch_gen_corr_l<2>(c, ga, blocks);
-        default: return launch_gen_corr_l<1>(c, ga, blocks);
+    const bool p2 = (c->gp.Ms & (c->gp.Ms - 1)) == 0;
+    switch (c->gp.L * 2 + (p2 ? 1 : 0)) {
+        case 17: return launch_gen_corr_l<8, true>(c, ga, blocks);
+        case 16: return launch_gen_corr_l<8, false>(c, ga, blocks);
+        case 9: return launch_gen_corr_l<4, true>(c, ga, blocks);
+        case 8: return launch_gen_corr_l<4, false>(c, ga, blocks);
+        case 5: return launch_gen_corr_l<2, true>(c, ga, blocks);
+        case 4: return launch_gen_corr_l<2, false>(c, ga, blocks);
+        case 3: return launch_gen_corr_l<1, true>(c, ga, blocks);
+        default: return launch_gen_corr_l<1, false>(c, ga, blocks);
     }
 }
 
@@ -356,14 +453,19 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         cx* Zp = reinterpret_cast<cx*>(c->d_Z);
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
         GenArgs ga{(const float2*)in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
-                   pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->logM, c->n_prn, c->radius};
-        const int gen_l = gen_split(c->logM), gen_sm = gen_smem(c->logM);
+                   pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->n_prn, c->radius, c->gp.M, c->gp.Ms,
+                   c->gp.n_pass, c->gp.sched()};
+        const int gen_l = c->gp.L, gen_sm = gen_smem(c->gp.Ms);
         if (c->gen) {
             const unsigned nb = (unsigned)(np * c->R * gen_l);
-            if (gen_l == 8) gacq_gen_fwd_kernel<8><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
-            else if (gen_l == 4) gacq_gen_fwd_kernel<4><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
-            else if (gen_l == 2) gacq_gen_fwd_kernel<2><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
-            else gacq_gen_fwd_kernel<1><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);
+            const bool p2 = (c->gp.Ms & (c->gp.Ms - 1)) == 0;
+#define GACQ_GEN_FWD(LL)                                                                               \
+    if (gen_l == LL) {                                                                                  \
+        if (p2) gacq_gen_fwd_kernel<LL, true><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);              \
+        else gacq_gen_fwd_kernel<LL, false><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);                \
+    }
+            GACQ_GEN_FWD(1) GACQ_GEN_FWD(2) GACQ_GEN_FWD(4) GACQ_GEN_FWD(8)
+#undef GACQ_GEN_FWD
             CUDA_TRY(cudaGetLastError());
         } else {
             const int fmt = fused_q ? inp.fmt : kFmtComplex64;
@@ -511,22 +613,13 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         }
     }
     const bool gen = !aligned || (p->plan_flags & GACQ_PLAN_GENERIC);
-    int logM = 0;
-    if (gen) {
-        // n_coh a power of two: the reference's n_coh-point circular correlation is the M = n_coh
-        // transform itself (no extension); otherwise the linear form with M >= n_coh + P - 1
-        while ((int64_t(1) << logM) < n_coh) ++logM;
-        if ((int64_t(1) << logM) != n_coh)
-            while ((int64_t(1) << logM) < n_coh + P - 1) ++logM;
-        logM = std::max(logM, 4);
-        if (logM > kGenMaxLogMTotal)
-            return fail(GACQ_ERR_UNSUPPORTED,
-                        "fs=%.17g Hz, coherent_ms=%d: the generic path's transform (%lld points >= n_coh + P - 1) "
-                        "exceeds %d (clusters of %d CTAs x %d points); chip-aligned rates (fs = D*1.023 MHz, "
-                        "D <= 16) take the prime-factor path",
-                        fs, p->coherent_ms, (long long)(int64_t(1) << logM), kGenMaxL * kGenMaxMs, kGenMaxL,
-                        kGenMaxMs);
-    }
+    GenPlan gp;
+    if (gen && !gen_plan(n_coh, P, gp))
+        return fail(GACQ_ERR_UNSUPPORTED,
+                    "fs=%.17g Hz, coherent_ms=%d: the generic path's transform (n_coh = %lld is not 2^a 3^b 5^c "
+                    "within %d points, and n_coh + P - 1 = %lld exceeds %d); chip-aligned rates "
+                    "(fs = D*1.023 MHz, D <= 16) take the prime-factor path",
+                    fs, p->coherent_ms, (long long)n_coh, kGenMaxM, (long long)(n_coh + P - 1), kGenMaxM);
     const int D = gen ? 0 : (int)(P / 1023), K = gen ? 0 : (int)(n_coh / P);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -547,7 +640,7 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     c->n_prn = p->n_prn;
     c->radius = p->exclusion_radius_samples ? p->exclusion_radius_samples : (int)std::ceil(fs / kChipRate);
     c->gen = gen;
-    c->logM = logM;
+    c->gp = gp;
     c->bins.assign(p->doppler_bins_hz, p->doppler_bins_hz + p->n_bins);
     c->prns.assign(p->prns, p->prns + p->n_prn);
 
@@ -564,10 +657,10 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     // in float64 then rounded once; twiddles (cos, sin)(2 pi e / M)
     std::vector<float2> gcc, gtw;
     if (gen) {
-        const int M = 1 << logM;
+        const int M = gp.M;
         gcc.resize((size_t)c->n_prn * M);
-        gtw.resize(M / 2);
-        for (int e = 0; e < M / 2; ++e)
+        gtw.resize(M);  // full table: M need not be even on the native path
+        for (int e = 0; e < M; ++e)
             gtw[e] = make_float2((float)std::cos(kTwoPi * e / M), (float)std::sin(kTwoPi * e / M));
         std::vector<int32_t> idx(n_coh);
         for (int64_t n = 0, ph = 0; n < n_coh; ++n) {
@@ -585,8 +678,9 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
                     ca_code(c->prns[i], chips);
                     std::fill(d.begin(), d.end(), 0.0);
                     for (int64_t n = 0; n < n_coh; ++n) d[n] = (double)chips[idx[n]];
-                    fft_f64(d);
-                    const int L = gen_split(logM), Ms = M / L;  // residue-major (gacq_generic.cuh)
+                    if (gp.native) dft_f64_rec(d.data(), M);
+                    else fft_f64(d);
+                    const int L = gp.L, Ms = gp.Ms;  // residue-major (gacq_generic.cuh)
                     for (int k = 0; k < M; ++k) {
                         const auto v = std::conj(d[k]) / (double)M;
                         gcc[(size_t)i * M + (k % L) * Ms + k / L] = make_float2((float)v.real(), (float)v.imag());
@@ -647,14 +741,19 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaMalloc(&c->d_gtw, gtw.size() * sizeof(float2)));
         CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-        const int sm_max = gen_smem(kGenMaxLogMs);
-        for (const void* k : {(const void*)gacq_gen_fwd_kernel<1>, (const void*)gacq_gen_fwd_kernel<2>,
-                              (const void*)gacq_gen_fwd_kernel<4>, (const void*)gacq_gen_fwd_kernel<8>,
-                              (const void*)gacq_gen_corr_kernel<1>, (const void*)gacq_gen_corr_kernel<2>,
-                              (const void*)gacq_gen_corr_kernel<4>, (const void*)gacq_gen_corr_kernel<8>})
+        const int sm_max = gen_smem(kGenMaxMs);
+        for (const void* k :
+             {(const void*)gacq_gen_fwd_kernel<1, true>, (const void*)gacq_gen_fwd_kernel<2, true>,
+              (const void*)gacq_gen_fwd_kernel<4, true>, (const void*)gacq_gen_fwd_kernel<8, true>,
+              (const void*)gacq_gen_corr_kernel<1, true>, (const void*)gacq_gen_corr_kernel<2, true>,
+              (const void*)gacq_gen_corr_kernel<4, true>, (const void*)gacq_gen_corr_kernel<8, true>,
+              (const void*)gacq_gen_fwd_kernel<1, false>, (const void*)gacq_gen_fwd_kernel<2, false>,
+              (const void*)gacq_gen_fwd_kernel<4, false>, (const void*)gacq_gen_fwd_kernel<8, false>,
+              (const void*)gacq_gen_corr_kernel<1, false>, (const void*)gacq_gen_corr_kernel<2, false>,
+              (const void*)gacq_gen_corr_kernel<4, false>, (const void*)gacq_gen_corr_kernel<8, false>})
             CTX_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max));
     }
-    const int64_t pair_bytes = (int64_t)c->R * (gen ? ((int64_t)1 << logM) : (int64_t)c->D * kSpec) *
+    const int64_t pair_bytes = (int64_t)c->R * (gen ? (int64_t)gp.M : (int64_t)c->D * kSpec) *
                                (int64_t)sizeof(float2);
     const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
@@ -699,7 +798,7 @@ int gacq_info_get(const gacq_ctx* c, gacq_info* o) {
     o->samples_per_period = c->P;
     o->n_coh = c->n_coh;
     o->chip_oversample = c->D;
-    o->fft_len = c->gen ? (1 << c->logM) : kChips;
+    o->fft_len = c->gen ? c->gp.M : kChips;
     o->n_bins = c->B;
     o->n_prn = c->n_prn;
     o->rounds = c->R;

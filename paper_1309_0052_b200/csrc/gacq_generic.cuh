@@ -1,27 +1,28 @@
 // gacq_generic.cuh -- the acquisition hot path at sample rates that are NOT chip-aligned
-// (fs != D * 1.023 MHz, e.g. 2.5 / 5 / 6 / 8.192 MHz front ends).
+// (fs != D * 1.023 MHz, e.g. 2.5 / 5 / 6 / 8.192 / 20 MHz front ends).
 //
 // Reference path: gnssperf/acquisition.py:112-159 with its native transform length
 // N = n_coh = round(fs * coherent_ms * 1e-3) and P = round(fs * 1023 / 1.023e6) lags.
-// Without chip alignment the polyphase reduction of gacq_pfa.cuh does not apply, so the
-// reference's N-point circular correlation is evaluated exactly as a linear correlation with
-// one power-of-two transform of M >= N + P - 1 points:
-//   r[tau] = sum_{n<N} c[n] w[(n + tau) mod N] = sum_n c[n] w_ext[n + tau],  tau < P,
-//   w_ext[j] = w[j mod N] (j < N + P - 1), zero beyond,   c = the sampled code replica
-//   r = IDFT_M( DFT_M(w_ext) . conj(DFT_M(c)) / M )[0, P)      (no index wrap for tau < P)
-// so no rescale is needed (the reference's ifft carries 1/N, the table carries 1/M).
-// When N is itself a power of two (e.g. 8.192 MHz) the plan takes M = N: the transform is then
-// the reference's circular correlation directly (j < M = N never reaches the extension).
+// Without chip alignment the polyphase reduction of gacq_pfa.cuh does not apply. The
+// reference's N-point circular correlation
+//   r[tau] = IDFT_N( DFT_N(w) . conj(DFT_N(c)) )[tau],  tau < P   (dsp.py:108-119: 1/N in the ifft)
+// is evaluated with one transform of M points:
+//   - native (M = N), when N = 2^a 3^b 5^c: mixed-radix (16/8/4/2, 5, 3) transforms at the
+//     reference's own length, no padding (5 MHz: 5000 points, 20 MHz: 20000);
+//   - otherwise linear (M = 2^k >= N + P - 1): r[tau] = sum_n c[n] w_ext[n + tau] with
+//     w_ext[j] = w[j mod N] (j < N + P - 1), zero beyond, so no lag wraps for tau < P.
+// The code table carries conj(DFT_M(c)) / M, so no rescale is needed in either form.
 //
 //   K1 gacq_gen_fwd_kernel : per (snapshot, bin, round): bit-exact wipe-off (kernels.py:78-86),
-//                            periodic extension, zero padding, forward M-point FFT -> Z.
+//                            periodic extension / zero padding (linear form), forward FFT -> Z.
 //   K2 gacq_gen_corr_kernel: per (snapshot, bin, PRN): for every round Z . Cg on load, inverse
-//                            FFT, |.|^2 of the first P lags accumulated in registers; first
-//                            argmax and exclusion floor (acquisition.py:151-159).
-// Both transforms are Stockham passes in shared memory (below). A CTA transforms at most
-// kGenMaxMs = 8192 points (16 values per thread across a pass's barrier: no spills); larger M is
-// split by one radix-L step over a cluster of L = M / 8192 CTAs (L <= 8, M <= 65536):
-//   forward, CTA l < L:  X[L k' + l] = DFT_Ms( sum_m x[n + m Ms] W_L^(-l m) W_M^(-l n) ),  Ms = M / L
+//                            FFT, |.|^2 of the P lags accumulated; first argmax and exclusion
+//                            floor (acquisition.py:151-159).
+// Both transforms are Stockham passes in shared memory (below), the radix schedule planned on
+// the host (GenArgs.radix). A CTA transforms at most 8192 points (7680 with radix 3 or 5
+// passes: 16 values per thread across a pass's barrier); a larger M is split by one radix-L
+// step over a cluster of L CTAs (L in {2, 4, 8}, L | M, Ms = M / L):
+//   forward, CTA l < L:  X[L k' + l] = DFT_Ms( sum_m x[n + m Ms] W_L^(-l m) W_M^(-l n) )
 //   inverse, CTA l:      E_l = IDFT_Ms(Y[L k' + l]), then each CTA takes a contiguous share of the
 //                        lags and combines r[tau] = sum_l W_M^(l tau) E_l[tau mod Ms], reading the
 //                        other CTAs' E_l straight from their shared memory (distributed shared
@@ -32,35 +33,33 @@
 #include <cstdint>
 
 #include "gacq_kernels.cuh"
+#include "rader31.cuh"  // r_dft5
+#include "pfa.cuh"      // dft3_fma
 
 namespace gacq {
 
-constexpr int kGenMaxLogMs = 13;
-constexpr int kGenMaxMs = 1 << kGenMaxLogMs;        // points per CTA transform
-constexpr int kGenMaxL = 8;                         // CTAs per cluster (portable cluster size)
-constexpr int kGenMaxLogMTotal = kGenMaxLogMs + 3;  // M <= 65536
+constexpr int kGenMaxMs = 8192;          // points per CTA transform (power-of-two schedules)
+constexpr int kGenMaxMsOdd = 7680;       // ... with a radix-3 or radix-5 pass (5 x 3 values per thread)
+constexpr int kGenMaxL = 8;              // CTAs per cluster (portable cluster size)
+constexpr int kGenMaxM = kGenMaxL * kGenMaxMs;
 constexpr int kGenThreads = 512;
-constexpr int kGenVPT = kGenMaxMs / kGenThreads;    // values per thread per pass (16)
-constexpr int kGenLags = kGenMaxMs / kGenThreads;   // lags per thread: a CTA's share of P is <= Ms
-__host__ __device__ constexpr int gen_split(int logM) { return logM > kGenMaxLogMs ? 1 << (logM - kGenMaxLogMs) : 1; }
-// the CTA transform's twiddles W_Ms^e, e < Ms/2, copied into shared memory once per CTA: the
-// Stockham passes read them there instead of from global memory (long-scoreboard stalls)
-__host__ __device__ constexpr int gen_tws_bytes(int logM) { return (int)sizeof(float2) * ((1 << logM) / gen_split(logM) / 2); }
-// dynamic smem of both generic kernels: one padded CTA transform (gpad), then (correlation
-// kernel) the power accumulators of the CTA's lags, <= Ms floats: in shared memory rather than
-// registers, where they would stay live across the transform and spill; then the twiddles
-__host__ __device__ constexpr int gen_smem(int logM) {
-    return (int)sizeof(float2) * ((1 << logM) / gen_split(logM) + (1 << logM) / gen_split(logM) / 16) +
-           (int)sizeof(float) * ((1 << logM) / gen_split(logM)) + gen_tws_bytes(logM);
+constexpr int kGenVPT = 16;              // values per thread per pass (at most)
+constexpr int kGenLags = kGenMaxMs / kGenThreads;  // lags per thread: a CTA's share of P is <= Ms
+constexpr int kGenMaxPasses = 16;  // 4-bit radix codes in a 64-bit schedule
+
+// dynamic smem of both generic kernels: one padded CTA transform (gpad), the power accumulators
+// of the CTA's lags (<= Ms floats; shared memory rather than registers, where they would stay
+// live across the transform and spill), and the CTA transform's twiddles W_Ms^e, e < Ms, copied
+// from the plan's W_M table once per CTA (global-table reads were the top stall)
+__host__ __device__ constexpr int gen_smem(int Ms) {
+    return (int)sizeof(float2) * (Ms + Ms / 16) + (int)sizeof(float) * Ms + (int)sizeof(float2) * Ms;
 }
 
-// (cos, S sin)(2 pi e / M) for any e in [0, M) from the half table (W^(e + M/2) = -W^e)
+// (cos, S sin)(2 pi e / T) from a full table of T entries
 template <int S>
-__device__ __forceinline__ cx gen_tw(const float2* __restrict__ tw, int e, int M) {
-    const bool hi = e >= (M >> 1);
-    const float2 t = tw[hi ? e - (M >> 1) : e];  // shared-memory table in the passes, global otherwise
-    const float c = hi ? -t.x : t.x, sn = hi ? -t.y : t.y;
-    return pk(c, S < 0 ? -sn : sn);
+__device__ __forceinline__ cx gen_tw(const float2* __restrict__ tw, int e) {
+    const float2 t = tw[e];  // shared-memory table in the passes, the global W_M table otherwise
+    return pk(t.x, S < 0 ? -t.y : t.y);
 }
 
 template <int S, int R>
@@ -69,8 +68,12 @@ __device__ __forceinline__ void gen_dft(cx (&v)[R]) {
         dft16<S>(v);
     } else if constexpr (R == 8) {
         dft8<S>(v);
+    } else if constexpr (R == 5) {
+        r_dft5<S>(v[0], v[1], v[2], v[3], v[4]);
     } else if constexpr (R == 4) {
         dft4<S>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 3) {
+        dft3_fma<S>(v);
     } else {
         const cx a = v[0];
         v[0] = add2(a, v[1]);
@@ -78,23 +81,22 @@ __device__ __forceinline__ void gen_dft(cx (&v)[R]) {
     }
 }
 
-// One Stockham autosort pass of radix R over x[0, Ms) (natural order in, natural order out
-// after the last pass), in place: every thread reads and transforms its groups, the CTA
-// synchronises, then every thread writes. Group j < Ms/R reads x[j + r Ms/R], applies
-// W_(Ns R)^(S k r), k = j mod Ns, and writes x[(j / Ns) Ns R + k + r Ns]. The twiddle table
-// is the plan's W_M half table, M = L Ms (W_(Ns R)^e = W_M^(e L Ms / (Ns R))).
 // Stockham buffers are padded: element i lives at i + i/16 (the radix-16 write pattern
 // x[16 j' + r] would otherwise put a warp's 32 stores into one bank group)
 __device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
 
-// kLoad: the first pass (logNs = 0, no twiddles) takes its inputs from load(i) instead of x[i]
-template <int S, int R, int VPT, bool kLoad = false, class Load = int>
-__device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs, int logNs,
-                                                  const float2* __restrict__ tw, int L, Load&& load = 0) {
-    constexpr int kGroups = VPT / R;  // VPT values per thread (Ms <= VPT * blockDim)
-    constexpr int kLogR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
-    const int Ms = 1 << logMs, ng = Ms >> kLogR, Ns = 1 << logNs;
-    const int tw_step = L << (logMs - logNs - kLogR);  // W_(Ns R) in units of W_M
+// One Stockham autosort pass of radix R over x[0, Ms) (natural order in, natural order out
+// after the last pass), in place: every thread reads and transforms its groups, the CTA
+// synchronises, then every thread writes. Group j < Ms/R reads x[j + r Ms/R], applies
+// W_(Ns R)^(S k r), k = j mod Ns (Ns = product of the earlier radices), and writes
+// x[(j / Ns) Ns R + k + r Ns]. `tw` is the W_Ms table (W_(Ns R)^e = W_Ms^(e Ms / (Ns R))).
+// kLoad: the first pass (Ns = 1, no twiddles) takes its inputs from load(i) instead of x[i].
+template <int S, int R, bool kLoad = false, class Load = int>
+__device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, int Ns, const float2* __restrict__ tw,
+                                                  Load&& load = 0) {
+    constexpr int kGroups = kGenVPT / R;  // groups per thread (Ms <= R kGroups blockDim)
+    const int ng = Ms / R, tw_step = Ms / (Ns * R);
+    const bool pow2 = (Ns & (Ns - 1)) == 0;  // shifts, not divisions, while only radix-2^k passes preceded
     cx v[kGroups][R];
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
@@ -107,20 +109,80 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs,
                 else
                     v[g][r] = x[gpad(j + r * ng)];
             }
-            const int k = j & (Ns - 1);
-            if (logNs > 0) {
+            if (!kLoad && Ns > 1) {
+                const int e1 = (pow2 ? j & (Ns - 1) : j % Ns) * tw_step;
                 // W^r from the table powers W^1, W^2, W^4, W^8 and at most two products each
                 // (<= 3 roundings per twiddle): 4 loads instead of R - 1
-                const int Mt = L << logMs, e1 = k * tw_step;
                 cx w[R];
-                w[1] = gen_tw<S>(tw, e1, Mt);
-                if (R > 2) w[2] = gen_tw<S>(tw, 2 * e1, Mt);
-                if (R > 4) w[4] = gen_tw<S>(tw, 4 * e1, Mt);
-                if (R > 8) w[8] = gen_tw<S>(tw, 8 * e1, Mt);
+                w[1] = gen_tw<S>(tw, e1);
+                if (R > 2) w[2] = gen_tw<S>(tw, 2 * e1);
+                if (R > 4 && R != 5) w[4] = gen_tw<S>(tw, 4 * e1);
+                if (R > 8) w[8] = gen_tw<S>(tw, 8 * e1);
 #pragma unroll
                 for (int r = 3; r < R; ++r) {
+                    if (R == 5) {  // W^3 = W^1 W^2, W^4 = W^2 W^2
+                        w[r] = r == 3 ? cmul(w[1], w[2]) : cmul(w[2], w[2]);
+                        continue;
+                    }
                     if ((r & (r - 1)) == 0) continue;  // powers of two are loaded
                     const int hb = r & 8 ? 8 : r & 4 ? 4 : 2;  // highest loaded power below r
+                    const int rest = r - hb;
+                    const int hb2 = rest & 4 ? 4 : rest & 2 ? 2 : 1;
+                    w[r] = rest == hb2 ? cmul(w[hb], w[rest]) : cmul(cmul(w[hb], w[hb2]), w[rest - hb2]);
+                }
+#pragma unroll
+                for (int r = 1; r < R; ++r) v[g][r] = cmul(v[g][r], w[r]);
+            }
+            gen_dft<S, R>(v[g]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+        const int j = threadIdx.x + g * blockDim.x;
+        if (j < ng) {
+            const int k = pow2 ? j & (Ns - 1) : j % Ns;
+            const int d = (j - k) * R + k;  // (j / Ns) Ns R + k
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[gpad(d + r * Ns)] = v[g][r];
+        }
+    }
+    __syncthreads();
+}
+
+// Power-of-two CTA transforms (Ms = 2^logMs): the same pass with shifts for every index, radix 16
+// and one 8/4/2 tail, the first (radix-16, twiddle-free) pass reading load(i) for x[i]. Inlined
+// with compile-time radices this measured 19% faster than the general schedule at 8192 points.
+template <int S, int R, bool kLoad = false, class Load = int>
+__device__ __forceinline__ void gen_p2_pass(cx* __restrict__ x, int logMs, int logNs, const float2* __restrict__ tw,
+                                            Load&& load = 0) {
+    constexpr int kGroups = kGenVPT / R;
+    constexpr int kLogR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
+    const int ng = (1 << logMs) >> kLogR, Ns = 1 << logNs;
+    const int tw_step = 1 << (logMs - logNs - kLogR);  // W_(Ns R) in units of W_Ms
+    cx v[kGroups][R];
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) {
+        const int j = threadIdx.x + g * blockDim.x;
+        if (j < ng) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if constexpr (kLoad)
+                    v[g][r] = load(j + r * ng);
+                else
+                    v[g][r] = x[gpad(j + r * ng)];
+            }
+            if (!kLoad && logNs > 0) {
+                const int e1 = (j & (Ns - 1)) * tw_step;
+                cx w[R];
+                w[1] = gen_tw<S>(tw, e1);
+                if (R > 2) w[2] = gen_tw<S>(tw, 2 * e1);
+                if (R > 4) w[4] = gen_tw<S>(tw, 4 * e1);
+                if (R > 8) w[8] = gen_tw<S>(tw, 8 * e1);
+#pragma unroll
+                for (int r = 3; r < R; ++r) {
+                    if ((r & (r - 1)) == 0) continue;
+                    const int hb = r & 8 ? 8 : r & 4 ? 4 : 2;
                     const int rest = r - hb;
                     const int hb2 = rest & 4 ? 4 : rest & 2 ? 2 : 1;
                     w[r] = rest == hb2 ? cmul(w[hb], w[rest]) : cmul(cmul(w[hb], w[hb2]), w[rest - hb2]);
@@ -144,42 +206,84 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int logMs,
     }
     __syncthreads();
 }
-
-// As gen_fft_stockham, with the first (radix-16, twiddle-free) pass reading load(i) for x[i]:
-// the inputs come straight from global memory, saving one shared-memory round trip and a barrier.
-template <int S, int VPT, class Load>
-__device__ __forceinline__ void gen_fft_stockham_ld(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, int L,
-                                                    Load&& load) {
-    gen_stockham_pass<S, 16, VPT, true>(x, logMs, 0, tw, L, load);
+template <int S, class Load>
+__device__ __forceinline__ void gen_p2_fft_ld(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, Load&& load) {
+    gen_p2_pass<S, 16, true>(x, logMs, 0, tw, load);
     int logNs = 4;
-    for (; logNs + 4 <= logMs; logNs += 4) gen_stockham_pass<S, 16, VPT>(x, logMs, logNs, tw, L);
+    for (; logNs + 4 <= logMs; logNs += 4) gen_p2_pass<S, 16>(x, logMs, logNs, tw);
     const int rem = logMs - logNs;
-    if (rem == 3) gen_stockham_pass<S, 8, VPT>(x, logMs, logNs, tw, L);
-    else if (rem == 2) gen_stockham_pass<S, 4, VPT>(x, logMs, logNs, tw, L);
-    else if (rem == 1) gen_stockham_pass<S, 2, VPT>(x, logMs, logNs, tw, L);
+    if (rem == 3) gen_p2_pass<S, 8>(x, logMs, logNs, tw);
+    else if (rem == 2) gen_p2_pass<S, 4>(x, logMs, logNs, tw);
+    else if (rem == 1) gen_p2_pass<S, 2>(x, logMs, logNs, tw);
 }
 
 struct GenArgs {
     const float2* snaps;    // batch base (device), snapshot s at snaps + s*stride
     int64_t stride;         // complex samples between snapshots
     const float2* carrier;  // [B][n_coh] wipe-off replicas
-    const float2* tw;       // [M/2] (cos, sin)(2 pi e / M)
+    const float2* tw;       // [M] (cos, sin)(2 pi e / M)
     const cx* Cg;           // [n_prn][M] conj(DFT_M(code replica)) / M, residue-major
     cx* Z;                  // [pairs_in_chunk][R][M] spectra, residue-major
     gacq_row* rows_bin;     // [n_snap][n_prn][B]
     float* pmap;            // optional [n_prn][B][P] (single snapshot), else null
     int* bad;               // atomicMin'd to the index of a snapshot holding a non-finite sample
     int64_t pair0;          // first (snapshot, bin) pair of this chunk
-    int B, R, n_coh, P, logM, n_prn, radius;  // M = 2^logM in total, L = 1 or 2 CTA-sized parts
+    int B, R, n_coh, P, n_prn, radius;
+    int M, Ms;              // transform length, points per CTA (M = L Ms)
+    int n_pass;             // Stockham passes of the Ms-point CTA transform
+    unsigned long long sched;  // their radices, 4 bits each from bit 0: gen_radix_code
 };
 
+// 4-bit codes of the pass radices in GenArgs.sched
+__host__ __device__ constexpr int gen_radix_code(int R) { return R == 16 ? 6 : R == 8 ? 5 : R == 5 ? 4 : R == 4 ? 3 : R == 3 ? 2 : 1; }
+__host__ __device__ constexpr int gen_code_radix(int c) { return c == 6 ? 16 : c == 5 ? 8 : c == 4 ? 5 : c == 3 ? 4 : c == 2 ? 3 : 2; }
 
-// grid: pairs_in_chunk * R * L CTAs of kGenThreads (part l = blockIdx.x % L); dynamic smem gen_smem
-template <int L>
+// Every pass as an out-of-line function: each gets its own register allocation (inlined into
+// the runtime radix switch, the kernels spilled the values a pass holds across its barrier)
+template <int S, int R>
+__device__ __noinline__ void gen_pass_call(cx* __restrict__ x, int Ms, int Ns, const float2* __restrict__ tw) {
+    gen_stockham_pass<S, R>(x, Ms, Ns, tw);
+}
+// first pass of the correlation kernel: inputs Z . Cg straight from global memory
+template <int R>
+__device__ __noinline__ void gen_first_pass_zc(cx* __restrict__ x, int Ms, const cx* __restrict__ z,
+                                               const cx* __restrict__ cg) {
+    gen_stockham_pass<1, R, true>(x, Ms, 1, nullptr, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cg[k])); });
+}
+
+// In-place natural-order DFT of x[0, Ms) (sign S, unnormalised) by the plan's Stockham passes,
+// starting at pass p0 with Ns = the product of the radices before it (mixed-radix schedules;
+// power-of-two ones take gen_p2_fft_ld).
+template <int S>
+__device__ __forceinline__ void gen_fft_from(cx* __restrict__ x, const GenArgs& a, int Ms, const float2* __restrict__ tw,
+                                             int p0, int Ns) {
+    for (int p = p0; p < a.n_pass; ++p) {
+        const int R = gen_code_radix((int)((a.sched >> (4 * p)) & 15));
+        switch (R) {
+            case 16: gen_pass_call<S, 16>(x, Ms, Ns, tw); break;
+            case 8: gen_pass_call<S, 8>(x, Ms, Ns, tw); break;
+            case 5: gen_pass_call<S, 5>(x, Ms, Ns, tw); break;
+            case 4: gen_pass_call<S, 4>(x, Ms, Ns, tw); break;
+            case 3: gen_pass_call<S, 3>(x, Ms, Ns, tw); break;
+            default: gen_pass_call<S, 2>(x, Ms, Ns, tw); break;
+        }
+        Ns *= R;
+    }
+}
+
+// shared-memory layout of both kernels: [transform (gpad)][Ms float accumulators][Ms twiddles]
+__device__ __forceinline__ float* gen_acc(cx* sm, int Ms) { return reinterpret_cast<float*>(sm + Ms + Ms / 16); }
+__device__ __forceinline__ float2* gen_tws(cx* sm, int Ms) { return reinterpret_cast<float2*>(gen_acc(sm, Ms) + Ms); }
+// W_Ms^e = W_M^(e L), e < Ms, into shared memory
+__device__ __forceinline__ void gen_load_tws(float2* tws, const float2* __restrict__ tw, int Ms, int L) {
+    for (int e = threadIdx.x; e < Ms; e += blockDim.x) tws[e] = __ldg(&tw[e * L]);
+}
+
+// grid: pairs_in_chunk * R * L CTAs of kGenThreads (part l = blockIdx.x % L); dynamic smem gen_smem(Ms)
+template <int L, bool kP2>
 __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a) {
     extern __shared__ __align__(16) cx sm[];
-    const int M = 1 << a.logM, logMs = a.logM - (L == 8 ? 3 : L == 4 ? 2 : L == 2 ? 1 : 0), Ms = 1 << logMs;
-    const int N = a.n_coh;
+    const int M = a.M, Ms = a.Ms, N = a.n_coh;
     const int part = blockIdx.x % L, lr = blockIdx.x / L;
     const int lp = lr / a.R, rd = lr % a.R;
     const int64_t pair = a.pair0 + lp;
@@ -189,7 +293,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
     const cx* c = reinterpret_cast<const cx*>(a.carrier) + (int64_t)b * N;
     const int ext = N + a.P - 1;
     unsigned fin = 0x7f800000u;  // see fin_word
-    auto wext = [&](int j) {  // periodically extended, zero-padded wiped block
+    auto wext = [&](int j) {  // wiped block; periodically extended and zero-padded in the linear form
         if (j >= ext) return czero();
         const int n = j < N ? j : j - N;
         const cx xv = __ldg(&x[n]);
@@ -200,24 +304,30 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
         cx y = wext(j);
         if constexpr (L > 1) {
 #pragma unroll
-            for (int m = 1; m < L; ++m) y = add2(y, cmul(wext(j + m * Ms), gen_tw<-1>(a.tw, ((part * m) % L) * Ms, M)));
-            if (part) y = cmul(y, gen_tw<-1>(a.tw, part * j, M));
+            for (int m = 1; m < L; ++m) y = add2(y, cmul(wext(j + m * Ms), gen_tw<-1>(a.tw, ((part * m) % L) * Ms)));
+            if (part) y = cmul(y, gen_tw<-1>(a.tw, part * j));
         }
         return y;
     };
-    float2* tws = reinterpret_cast<float2*>(reinterpret_cast<float*>(sm + Ms + Ms / 16) + Ms);
-    for (int e = threadIdx.x; e < Ms / 2; e += blockDim.x) tws[e] = __ldg(&a.tw[e * L]);  // W_Ms^e = W_M^(e L)
+    float2* tws = gen_tws(sm, Ms);
+    gen_load_tws(tws, a.tw, Ms, L);
     __syncthreads();
-    gen_fft_stockham_ld<-1, kGenVPT>(sm, logMs, tws, 1, input);  // read straight into the first pass
+    if constexpr (kP2) {
+        gen_p2_fft_ld<-1>(sm, 31 - __clz(Ms), tws, input);  // read straight into the first pass
+    } else {
+        for (int i = threadIdx.x; i < Ms; i += blockDim.x) sm[gpad(i)] = input(i);  // staged (wipe, split)
+        __syncthreads();
+        gen_fft_from<-1>(sm, a, Ms, tws, 0, 1);
+    }
     if (__syncthreads_or(fin == 0u) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
     for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[gpad(k)];
 }
 
 // grid: pairs_in_chunk * n_prn * L CTAs of kGenThreads, clusters of L along x (item =
-// blockIdx.x / L = lp * n_prn + pi, part = cluster rank); dynamic smem gen_smem. CTA `part`
+// blockIdx.x / L = lp * n_prn + pi, part = cluster rank); dynamic smem gen_smem(Ms). CTA `part`
 // owns lags [part Pc, (part + 1) Pc), Pc = ceil(P / L), and their power accumulators.
-template <int L>
+template <int L, bool kP2>
 __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a) {
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) cx sm[];
@@ -225,41 +335,48 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     __shared__ int red_i[kGenThreads / 32];
     __shared__ float s_best, s_floor;
     __shared__ int s_bidx;
-    const int M = 1 << a.logM, logMs = a.logM - (L == 8 ? 3 : L == 4 ? 2 : L == 2 ? 1 : 0), Ms = 1 << logMs;
+    const int M = a.M, Ms = a.Ms;
     const int item = blockIdx.x / L, part = blockIdx.x % L;
     const int lp = item / a.n_prn, pi = item % a.n_prn;
     const cx* cgt = a.Cg + (int64_t)pi * M + (int64_t)part * Ms;
     const int Pc = (a.P + L - 1) / L, t0 = part * Pc, t1 = min(a.P, t0 + Pc);
     cg::cluster_group cl = cg::this_cluster();
-    float* acc = reinterpret_cast<float*>(sm + Ms + Ms / 16) + threadIdx.x;  // lag t0 + tid + i*512 at acc[i*512]
-    float2* tws = reinterpret_cast<float2*>(reinterpret_cast<float*>(sm + Ms + Ms / 16) + Ms);
-    for (int e = threadIdx.x; e < Ms / 2; e += blockDim.x) tws[e] = __ldg(&a.tw[e * L]);  // W_Ms^e = W_M^(e L)
+    float* acc = gen_acc(sm, Ms) + threadIdx.x;  // lag t0 + tid + i*512 at acc[i*512]
+    float2* tws = gen_tws(sm, Ms);
+    gen_load_tws(tws, a.tw, Ms, L);
 #pragma unroll
     for (int i = 0; i < kGenLags; ++i)
         if ((int)threadIdx.x + i * kGenThreads < Ms) acc[i * kGenThreads] = 0.f;  // the region holds Ms floats
+    __syncthreads();
     for (int rd = 0; rd < a.R; ++rd) {
-        // an opaque copy of logMs per round: the passes' thread-invariant addresses are then
-        // recomputed each round instead of hoisted out of the loop and held live (spills)
-        int lgs = logMs;
-        asm volatile("" : "+r"(lgs));
-        cx* const X = sm;
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
-        // Z . Cg read straight into the first pass (logMs >= 4 on this path)
-        gen_fft_stockham_ld<1, kGenVPT>(X, lgs, tws, 1, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cgt[k])); });
+        // Z . Cg read straight into the first pass
+        const int R0 = gen_code_radix((int)(a.sched & 15));
+        if constexpr (kP2) {  // Z . Cg read straight into the first pass
+            gen_p2_fft_ld<1>(sm, 31 - __clz(Ms), tws, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cgt[k])); });
+        } else if (R0 == 16 || R0 == 8) {  // ... out of line
+            if (R0 == 16) gen_first_pass_zc<16>(sm, Ms, z, cgt);
+            else gen_first_pass_zc<8>(sm, Ms, z, cgt);
+            gen_fft_from<1>(sm, a, Ms, tws, 1, R0);
+        } else {
+            for (int i = threadIdx.x; i < Ms; i += blockDim.x) sm[gpad(i)] = cmul(__ldg(&z[i]), __ldg(&cgt[i]));
+            __syncthreads();
+            gen_fft_from<1>(sm, a, Ms, tws, 0, 1);
+        }
         if constexpr (L > 1) cl.sync();  // every E_l complete
 #pragma unroll 2
         for (int i = 0; i < kGenLags; ++i) {
             const int t = t0 + threadIdx.x + i * kGenThreads;
             if (t < t1) {
-                const int e = gpad(t & (Ms - 1));
+                const int e = gpad(L == 1 ? t : t % Ms);
                 cx v;
                 if constexpr (L == 1) {
-                    v = X[e];
+                    v = sm[e];
                 } else {  // E_l of every CTA of the cluster (distributed shared memory)
-                    v = *cl.map_shared_rank(X + e, 0);
+                    v = *cl.map_shared_rank(sm + e, 0);
 #pragma unroll
                     for (int l = 1; l < L; ++l)
-                        v = add2(v, cmul(*cl.map_shared_rank(X + e, l), gen_tw<1>(a.tw, (l * t) & (M - 1), M)));
+                        v = add2(v, cmul(*cl.map_shared_rank(sm + e, l), gen_tw<1>(a.tw, (int)(((int64_t)l * t) % M))));
                 }
                 float& A = acc[i * kGenThreads];
                 A = fmaf(im(v), im(v), fmaf(re(v), re(v), A));  // acquisition.py:149

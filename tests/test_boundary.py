@@ -92,14 +92,15 @@ def test_buffer_validation_order_and_messages(pkg):
 
 
 def test_create_rejects_oversized_generic_rate_before_touching_a_device(pkg):
-    # 40 MHz is not chip-aligned and its generic transform (n_coh + P - 1 -> 131072 points)
-    # exceeds the 8-CTA cluster (8 x 8192 points): refused loudly, never a CPU path
+    # 40.1 MHz: n_coh = 40100 = 4 * 25 * 401 is not 2^a 3^b 5^c, and the power-of-two linear
+    # transform (n_coh + P - 1 -> 131072 points) exceeds the 8-CTA cluster (65536): refused
+    # loudly, never a CPU path
     with pytest.raises(pkg.UnsupportedError, match="generic path"):
-        pkg.AcqEngine(40e6, [1], pkg.AcqConfig())
-    # 20 MHz with 3 ms coherent: 60000 + 20000 - 1 points -> 131072, also refused (20 MHz at 1
-    # and 2 ms, 65536 points, run on the cluster)
+        pkg.AcqEngine(40.1e6, [1], pkg.AcqConfig())
+    # 16.367 MHz with 4 ms coherent: 65468 = 4 * 13 * 1259, linear form 81834 points: refused
+    # (2 ms, 32734 + 16367 - 1 -> 65536 points, runs)
     with pytest.raises(pkg.UnsupportedError, match="generic path"):
-        pkg.AcqEngine(20e6, [1], pkg.AcqConfig(coherent_ms=3))
+        pkg.AcqEngine(16.367e6, [1], pkg.AcqConfig(coherent_ms=4))
 
 
 def test_create_without_gpu_raises_resource_error(pkg):
