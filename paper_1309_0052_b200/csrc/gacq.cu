@@ -90,6 +90,7 @@ void ca_code(int prn, int8_t* out) {
 // power of two >= n_coh + P - 1 (linear); L CTAs of Ms = M / L points each (gacq_generic.cuh)
 struct GenPlan {
     int M = 0, L = 1, Ms = 0, n_pass = 0;
+    int T = 512;  // threads per CTA: 256 (two CTAs per SM) when two CTAs' shared memory fits
     bool native = false;
     signed char radix[gacq::kGenMaxPasses] = {};
     unsigned long long sched() const {
@@ -122,6 +123,8 @@ void gen_passes(GenPlan& g) {
     for (; m % 3 == 0; m /= 3) g.radix[g.n_pass++] = 3;
 }
 
+void gen_threads(GenPlan& g) { g.T = 2 * (gacq::gen_smem(g.Ms) + 2048) <= 228 * 1024 ? 256 : 512; }
+
 // false when no transform of at most kGenMaxM points serves (n_coh, P)
 bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
     if (smooth235(n_coh) && n_coh >= 16) {
@@ -135,6 +138,7 @@ bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
                 g.L = L;
                 g.Ms = (int)Ms;
                 gen_passes(g);
+                gen_threads(g);
                 return true;
             }
         }
@@ -147,6 +151,7 @@ bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
     g.L = (int)std::max<int64_t>(1, M / gacq::kGenMaxMs);
     g.Ms = (int)(M / g.L);
     gen_passes(g);
+    gen_threads(g);
     return true;
 }
 
@@ -296,12 +301,18 @@ cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     return cudaGetLastError();
 }
 
-// generic correlation: clusters of gp.L CTAs (distributed shared memory, gacq_generic.cuh)
-template <int L, bool kP2>
+// generic kernels: clusters of gp.L CTAs (distributed shared memory, gacq_generic.cuh) of gp.T
+// threads; every (L, power-of-two, T) instantiation through one dispatch
+#define GACQ_GEN_DISPATCH(F)                                                                       \
+    F(1, true, 256) F(1, false, 256) F(2, true, 256) F(2, false, 256) F(4, true, 256) F(4, false, 256) \
+    F(8, true, 256) F(8, false, 256) F(1, true, 512) F(1, false, 512) F(2, true, 512) F(2, false, 512) \
+    F(4, true, 512) F(4, false, 512) F(8, true, 512) F(8, false, 512)
+
+template <int L, bool kP2, int T>
 cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t blocks) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
-    cfg.blockDim = dim3(kGenThreads);
+    cfg.blockDim = dim3(T);
     cfg.dynamicSmemBytes = gen_smem(c->gp.Ms);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
@@ -311,20 +322,20 @@ cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t bloc
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gacq_gen_corr_kernel<L, kP2>, ga);
+    return cudaLaunchKernelEx(&cfg, gacq_gen_corr_kernel<L, kP2, T>, ga);
 }
-cudaError_t launch_gen_corr(const gacq_ctx* c, const GenArgs& ga, int64_t blocks) {
+cudaError_t launch_gen(const gacq_ctx* c, const GenArgs& ga, int64_t np, bool corr) {
     const bool p2 = (c->gp.Ms & (c->gp.Ms - 1)) == 0;
-    switch (c->gp.L * 2 + (p2 ? 1 : 0)) {
-        case 17: return launch_gen_corr_l<8, true>(c, ga, blocks);
-        case 16: return launch_gen_corr_l<8, false>(c, ga, blocks);
-        case 9: return launch_gen_corr_l<4, true>(c, ga, blocks);
-        case 8: return launch_gen_corr_l<4, false>(c, ga, blocks);
-        case 5: return launch_gen_corr_l<2, true>(c, ga, blocks);
-        case 4: return launch_gen_corr_l<2, false>(c, ga, blocks);
-        case 3: return launch_gen_corr_l<1, true>(c, ga, blocks);
-        default: return launch_gen_corr_l<1, false>(c, ga, blocks);
+    const int L = c->gp.L, T = c->gp.T;
+#define GACQ_GEN_LAUNCH(LL, PP, TT)                                                                          \
+    if (L == LL && p2 == PP && T == TT) {                                                                    \
+        if (corr) return launch_gen_corr_l<LL, PP, TT>(c, ga, np * c->n_prn * LL);                           \
+        gacq_gen_fwd_kernel<LL, PP, TT><<<(unsigned)(np * c->R * LL), TT, gen_smem(c->gp.Ms), c->stream>>>(ga); \
+        return cudaGetLastError();                                                                           \
     }
+    GACQ_GEN_DISPATCH(GACQ_GEN_LAUNCH)
+#undef GACQ_GEN_LAUNCH
+    return cudaErrorInvalidConfiguration;
 }
 
 cudaEvent_t prof_event(gacq_ctx* c, size_t i) {
@@ -455,18 +466,8 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         GenArgs ga{(const float2*)in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
                    pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->n_prn, c->radius, c->gp.M, c->gp.Ms,
                    c->gp.n_pass, c->gp.sched()};
-        const int gen_l = c->gp.L, gen_sm = gen_smem(c->gp.Ms);
         if (c->gen) {
-            const unsigned nb = (unsigned)(np * c->R * gen_l);
-            const bool p2 = (c->gp.Ms & (c->gp.Ms - 1)) == 0;
-#define GACQ_GEN_FWD(LL)                                                                               \
-    if (gen_l == LL) {                                                                                  \
-        if (p2) gacq_gen_fwd_kernel<LL, true><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);              \
-        else gacq_gen_fwd_kernel<LL, false><<<nb, kGenThreads, gen_sm, c->stream>>>(ga);                \
-    }
-            GACQ_GEN_FWD(1) GACQ_GEN_FWD(2) GACQ_GEN_FWD(4) GACQ_GEN_FWD(8)
-#undef GACQ_GEN_FWD
-            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(launch_gen(c, ga, np, false));
         } else {
             const int fmt = fused_q ? inp.fmt : kFmtComplex64;
             const double qs = inp.scale / (inp.fmt == GACQ_FMT_INT8 ? 127.0 : 32767.0);
@@ -477,7 +478,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (!c->gen) CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), c->stream));
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 1}); }
         if (c->gen) {
-            CUDA_TRY(launch_gen_corr(c, ga, np * c->n_prn * gen_l));
+            CUDA_TRY(launch_gen(c, ga, np, true));
         } else {
             const int64_t n_units = (np + kCorrWarps - 1) / kCorrWarps * c->n_prn;
             if (n_units + c->corr_slots >= INT32_MAX) return fail(GACQ_ERR_UNSUPPORTED, "chunk too large");
@@ -742,15 +743,12 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
         const int sm_max = gen_smem(kGenMaxMs);
-        for (const void* k :
-             {(const void*)gacq_gen_fwd_kernel<1, true>, (const void*)gacq_gen_fwd_kernel<2, true>,
-              (const void*)gacq_gen_fwd_kernel<4, true>, (const void*)gacq_gen_fwd_kernel<8, true>,
-              (const void*)gacq_gen_corr_kernel<1, true>, (const void*)gacq_gen_corr_kernel<2, true>,
-              (const void*)gacq_gen_corr_kernel<4, true>, (const void*)gacq_gen_corr_kernel<8, true>,
-              (const void*)gacq_gen_fwd_kernel<1, false>, (const void*)gacq_gen_fwd_kernel<2, false>,
-              (const void*)gacq_gen_fwd_kernel<4, false>, (const void*)gacq_gen_fwd_kernel<8, false>,
-              (const void*)gacq_gen_corr_kernel<1, false>, (const void*)gacq_gen_corr_kernel<2, false>,
-              (const void*)gacq_gen_corr_kernel<4, false>, (const void*)gacq_gen_corr_kernel<8, false>})
+        std::vector<const void*> ks;
+#define GACQ_GEN_KS(LL, PP, TT) \
+    ks.push_back((const void*)gacq_gen_fwd_kernel<LL, PP, TT>); ks.push_back((const void*)gacq_gen_corr_kernel<LL, PP, TT>);
+        GACQ_GEN_DISPATCH(GACQ_GEN_KS)
+#undef GACQ_GEN_KS
+        for (const void* k : ks)
             CTX_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_max));
     }
     const int64_t pair_bytes = (int64_t)c->R * (gen ? (int64_t)gp.M : (int64_t)c->D * kSpec) *

@@ -42,9 +42,10 @@ constexpr int kGenMaxMs = 8192;          // points per CTA transform (power-of-t
 constexpr int kGenMaxMsOdd = 7680;       // ... with a radix-3 or radix-5 pass (5 x 3 values per thread)
 constexpr int kGenMaxL = 8;              // CTAs per cluster (portable cluster size)
 constexpr int kGenMaxM = kGenMaxL * kGenMaxMs;
-constexpr int kGenThreads = 512;
-constexpr int kGenVPT = 16;              // values per thread per pass (at most)
-constexpr int kGenLags = kGenMaxMs / kGenThreads;  // lags per thread: a CTA's share of P is <= Ms
+// Threads per CTA: 256 (32 values per thread per pass, two CTAs per SM) when two CTAs' shared
+// memory fits an SM, else 512 (16 values per thread, one CTA per SM). A CTA's share of the lags
+// is <= Ms, so each thread owns at most kGenMaxMs / T of them.
+__host__ __device__ constexpr int gen_vpt(int T) { return kGenMaxMs / T; }
 constexpr int kGenMaxPasses = 16;  // 4-bit radix codes in a 64-bit schedule
 
 // dynamic smem of both generic kernels: one padded CTA transform (gpad), the power accumulators
@@ -91,12 +92,16 @@ __device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
 // W_(Ns R)^(S k r), k = j mod Ns (Ns = product of the earlier radices), and writes
 // x[(j / Ns) Ns R + k + r Ns]. `tw` is the W_Ms table (W_(Ns R)^e = W_Ms^(e Ms / (Ns R))).
 // kLoad: the first pass (Ns = 1, no twiddles) takes its inputs from load(i) instead of x[i].
-template <int S, int R, bool kLoad = false, class Load = int>
+template <int S, int R, int VPT, bool kLoad = false, class Load = int>
 __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, int Ns, const float2* __restrict__ tw,
                                                   Load&& load = 0) {
-    constexpr int kGroups = kGenVPT / R;  // groups per thread (Ms <= R kGroups blockDim)
+    constexpr int kGroups = VPT / R;  // groups per thread (Ms <= R kGroups blockDim)
     const int ng = Ms / R, tw_step = Ms / (Ns * R);
     const bool pow2 = (Ns & (Ns - 1)) == 0;  // shifts, not divisions, while only radix-2^k passes preceded
+    // j mod Ns otherwise by a multiply-high: floor(j m / 2^32) = floor(j / Ns) with
+    // m = ceil(2^32 / Ns), exact here since j Ns < 2^26
+    const unsigned magic = pow2 ? 0u : (unsigned)((0xffffffffull + Ns) / (unsigned)Ns);
+    auto jmod = [&](int j) { return pow2 ? j & (Ns - 1) : j - (int)__umulhi((unsigned)j, magic) * Ns; };
     cx v[kGroups][R];
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
@@ -110,7 +115,7 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
                     v[g][r] = x[gpad(j + r * ng)];
             }
             if (!kLoad && Ns > 1) {
-                const int e1 = (pow2 ? j & (Ns - 1) : j % Ns) * tw_step;
+                const int e1 = jmod(j) * tw_step;
                 // W^r from the table powers W^1, W^2, W^4, W^8 and at most two products each
                 // (<= 3 roundings per twiddle): 4 loads instead of R - 1
                 cx w[R];
@@ -141,7 +146,7 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
     for (int g = 0; g < kGroups; ++g) {
         const int j = threadIdx.x + g * blockDim.x;
         if (j < ng) {
-            const int k = pow2 ? j & (Ns - 1) : j % Ns;
+            const int k = jmod(j);
             const int d = (j - k) * R + k;  // (j / Ns) Ns R + k
 #pragma unroll
             for (int r = 0; r < R; ++r) x[gpad(d + r * Ns)] = v[g][r];
@@ -153,10 +158,10 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
 // Power-of-two CTA transforms (Ms = 2^logMs): the same pass with shifts for every index, radix 16
 // and one 8/4/2 tail, the first (radix-16, twiddle-free) pass reading load(i) for x[i]. Inlined
 // with compile-time radices this measured 19% faster than the general schedule at 8192 points.
-template <int S, int R, bool kLoad = false, class Load = int>
+template <int S, int R, int VPT, bool kLoad = false, class Load = int>
 __device__ __forceinline__ void gen_p2_pass(cx* __restrict__ x, int logMs, int logNs, const float2* __restrict__ tw,
                                             Load&& load = 0) {
-    constexpr int kGroups = kGenVPT / R;
+    constexpr int kGroups = VPT / R;
     constexpr int kLogR = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const int ng = (1 << logMs) >> kLogR, Ns = 1 << logNs;
     const int tw_step = 1 << (logMs - logNs - kLogR);  // W_(Ns R) in units of W_Ms
@@ -206,15 +211,15 @@ __device__ __forceinline__ void gen_p2_pass(cx* __restrict__ x, int logMs, int l
     }
     __syncthreads();
 }
-template <int S, class Load>
+template <int S, int VPT, class Load>
 __device__ __forceinline__ void gen_p2_fft_ld(cx* __restrict__ x, int logMs, const float2* __restrict__ tw, Load&& load) {
-    gen_p2_pass<S, 16, true>(x, logMs, 0, tw, load);
+    gen_p2_pass<S, 16, VPT, true>(x, logMs, 0, tw, load);
     int logNs = 4;
-    for (; logNs + 4 <= logMs; logNs += 4) gen_p2_pass<S, 16>(x, logMs, logNs, tw);
+    for (; logNs + 4 <= logMs; logNs += 4) gen_p2_pass<S, 16, VPT>(x, logMs, logNs, tw);
     const int rem = logMs - logNs;
-    if (rem == 3) gen_p2_pass<S, 8>(x, logMs, logNs, tw);
-    else if (rem == 2) gen_p2_pass<S, 4>(x, logMs, logNs, tw);
-    else if (rem == 1) gen_p2_pass<S, 2>(x, logMs, logNs, tw);
+    if (rem == 3) gen_p2_pass<S, 8, VPT>(x, logMs, logNs, tw);
+    else if (rem == 2) gen_p2_pass<S, 4, VPT>(x, logMs, logNs, tw);
+    else if (rem == 1) gen_p2_pass<S, 2, VPT>(x, logMs, logNs, tw);
 }
 
 struct GenArgs {
@@ -240,32 +245,32 @@ __host__ __device__ constexpr int gen_code_radix(int c) { return c == 6 ? 16 : c
 
 // Every pass as an out-of-line function: each gets its own register allocation (inlined into
 // the runtime radix switch, the kernels spilled the values a pass holds across its barrier)
-template <int S, int R>
+template <int S, int R, int VPT>
 __device__ __noinline__ void gen_pass_call(cx* __restrict__ x, int Ms, int Ns, const float2* __restrict__ tw) {
-    gen_stockham_pass<S, R>(x, Ms, Ns, tw);
+    gen_stockham_pass<S, R, VPT>(x, Ms, Ns, tw);
 }
 // first pass of the correlation kernel: inputs Z . Cg straight from global memory
-template <int R>
+template <int R, int VPT>
 __device__ __noinline__ void gen_first_pass_zc(cx* __restrict__ x, int Ms, const cx* __restrict__ z,
                                                const cx* __restrict__ cg) {
-    gen_stockham_pass<1, R, true>(x, Ms, 1, nullptr, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cg[k])); });
+    gen_stockham_pass<1, R, VPT, true>(x, Ms, 1, nullptr, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cg[k])); });
 }
 
 // In-place natural-order DFT of x[0, Ms) (sign S, unnormalised) by the plan's Stockham passes,
 // starting at pass p0 with Ns = the product of the radices before it (mixed-radix schedules;
 // power-of-two ones take gen_p2_fft_ld).
-template <int S>
+template <int S, int VPT>
 __device__ __forceinline__ void gen_fft_from(cx* __restrict__ x, const GenArgs& a, int Ms, const float2* __restrict__ tw,
                                              int p0, int Ns) {
     for (int p = p0; p < a.n_pass; ++p) {
         const int R = gen_code_radix((int)((a.sched >> (4 * p)) & 15));
         switch (R) {
-            case 16: gen_pass_call<S, 16>(x, Ms, Ns, tw); break;
-            case 8: gen_pass_call<S, 8>(x, Ms, Ns, tw); break;
-            case 5: gen_pass_call<S, 5>(x, Ms, Ns, tw); break;
-            case 4: gen_pass_call<S, 4>(x, Ms, Ns, tw); break;
-            case 3: gen_pass_call<S, 3>(x, Ms, Ns, tw); break;
-            default: gen_pass_call<S, 2>(x, Ms, Ns, tw); break;
+            case 16: gen_pass_call<S, 16, VPT>(x, Ms, Ns, tw); break;
+            case 8: gen_pass_call<S, 8, VPT>(x, Ms, Ns, tw); break;
+            case 5: gen_pass_call<S, 5, VPT>(x, Ms, Ns, tw); break;
+            case 4: gen_pass_call<S, 4, VPT>(x, Ms, Ns, tw); break;
+            case 3: gen_pass_call<S, 3, VPT>(x, Ms, Ns, tw); break;
+            default: gen_pass_call<S, 2, VPT>(x, Ms, Ns, tw); break;
         }
         Ns *= R;
     }
@@ -279,9 +284,10 @@ __device__ __forceinline__ void gen_load_tws(float2* tws, const float2* __restri
     for (int e = threadIdx.x; e < Ms; e += blockDim.x) tws[e] = __ldg(&tw[e * L]);
 }
 
-// grid: pairs_in_chunk * R * L CTAs of kGenThreads (part l = blockIdx.x % L); dynamic smem gen_smem(Ms)
-template <int L, bool kP2>
-__global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a) {
+// grid: pairs_in_chunk * R * L CTAs of T threads (part l = blockIdx.x % L); dynamic smem gen_smem(Ms)
+template <int L, bool kP2, int T>
+__global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_fwd_kernel(GenArgs a) {
+    constexpr int VPT = gen_vpt(T);
     extern __shared__ __align__(16) cx sm[];
     const int M = a.M, Ms = a.Ms, N = a.n_coh;
     const int part = blockIdx.x % L, lr = blockIdx.x / L;
@@ -313,26 +319,27 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_fwd_kernel(GenArgs a)
     gen_load_tws(tws, a.tw, Ms, L);
     __syncthreads();
     if constexpr (kP2) {
-        gen_p2_fft_ld<-1>(sm, 31 - __clz(Ms), tws, input);  // read straight into the first pass
+        gen_p2_fft_ld<-1, VPT>(sm, 31 - __clz(Ms), tws, input);  // read straight into the first pass
     } else {
         for (int i = threadIdx.x; i < Ms; i += blockDim.x) sm[gpad(i)] = input(i);  // staged (wipe, split)
         __syncthreads();
-        gen_fft_from<-1>(sm, a, Ms, tws, 0, 1);
+        gen_fft_from<-1, VPT>(sm, a, Ms, tws, 0, 1);
     }
     if (__syncthreads_or(fin == 0u) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
     for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[gpad(k)];
 }
 
-// grid: pairs_in_chunk * n_prn * L CTAs of kGenThreads, clusters of L along x (item =
+// grid: pairs_in_chunk * n_prn * L CTAs of T threads, clusters of L along x (item =
 // blockIdx.x / L = lp * n_prn + pi, part = cluster rank); dynamic smem gen_smem(Ms). CTA `part`
 // owns lags [part Pc, (part + 1) Pc), Pc = ceil(P / L), and their power accumulators.
-template <int L, bool kP2>
-__global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a) {
+template <int L, bool kP2, int T>
+__global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_kernel(GenArgs a) {
+    constexpr int VPT = gen_vpt(T), kLags = kGenMaxMs / T;
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) cx sm[];
-    __shared__ float red_v[kGenThreads / 32], red_f[kGenThreads / 32];
-    __shared__ int red_i[kGenThreads / 32];
+    __shared__ float red_v[T / 32], red_f[T / 32];
+    __shared__ int red_i[T / 32];
     __shared__ float s_best, s_floor;
     __shared__ int s_bidx;
     const int M = a.M, Ms = a.Ms;
@@ -345,28 +352,28 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     float2* tws = gen_tws(sm, Ms);
     gen_load_tws(tws, a.tw, Ms, L);
 #pragma unroll
-    for (int i = 0; i < kGenLags; ++i)
-        if ((int)threadIdx.x + i * kGenThreads < Ms) acc[i * kGenThreads] = 0.f;  // the region holds Ms floats
+    for (int i = 0; i < kLags; ++i)
+        if ((int)threadIdx.x + i * T < Ms) acc[i * T] = 0.f;  // the region holds Ms floats
     __syncthreads();
     for (int rd = 0; rd < a.R; ++rd) {
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
         // Z . Cg read straight into the first pass
         const int R0 = gen_code_radix((int)(a.sched & 15));
         if constexpr (kP2) {  // Z . Cg read straight into the first pass
-            gen_p2_fft_ld<1>(sm, 31 - __clz(Ms), tws, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cgt[k])); });
+            gen_p2_fft_ld<1, VPT>(sm, 31 - __clz(Ms), tws, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cgt[k])); });
         } else if (R0 == 16 || R0 == 8) {  // ... out of line
-            if (R0 == 16) gen_first_pass_zc<16>(sm, Ms, z, cgt);
-            else gen_first_pass_zc<8>(sm, Ms, z, cgt);
-            gen_fft_from<1>(sm, a, Ms, tws, 1, R0);
+            if (R0 == 16) gen_first_pass_zc<16, VPT>(sm, Ms, z, cgt);
+            else gen_first_pass_zc<8, VPT>(sm, Ms, z, cgt);
+            gen_fft_from<1, VPT>(sm, a, Ms, tws, 1, R0);
         } else {
             for (int i = threadIdx.x; i < Ms; i += blockDim.x) sm[gpad(i)] = cmul(__ldg(&z[i]), __ldg(&cgt[i]));
             __syncthreads();
-            gen_fft_from<1>(sm, a, Ms, tws, 0, 1);
+            gen_fft_from<1, VPT>(sm, a, Ms, tws, 0, 1);
         }
         if constexpr (L > 1) cl.sync();  // every E_l complete
 #pragma unroll 2
-        for (int i = 0; i < kGenLags; ++i) {
-            const int t = t0 + threadIdx.x + i * kGenThreads;
+        for (int i = 0; i < kLags; ++i) {
+            const int t = t0 + threadIdx.x + i * T;
             if (t < t1) {
                 const int e = gpad(L == 1 ? t : t % Ms);
                 cx v;
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
                     for (int l = 1; l < L; ++l)
                         v = add2(v, cmul(*cl.map_shared_rank(sm + e, l), gen_tw<1>(a.tw, (int)(((int64_t)l * t) % M))));
                 }
-                float& A = acc[i * kGenThreads];
+                float& A = acc[i * T];
                 A = fmaf(im(v), im(v), fmaf(re(v), re(v), A));  // acquisition.py:149
             }
         }
@@ -392,9 +399,9 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     float best = -1.f;
     int bidx = 0x7fffffff;
 #pragma unroll
-    for (int i = 0; i < kGenLags; ++i) {
-        const int t = t0 + threadIdx.x + i * kGenThreads;
-        if (t < t1 && better(acc[i * kGenThreads], t, best, bidx)) { best = acc[i * kGenThreads]; bidx = t; }
+    for (int i = 0; i < kLags; ++i) {
+        const int t = t0 + threadIdx.x + i * T;
+        if (t < t1 && better(acc[i * T], t, best, bidx)) { best = acc[i * T]; bidx = t; }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -429,13 +436,13 @@ __global__ void __launch_bounds__(kGenThreads, 1) gacq_gen_corr_kernel(GenArgs a
     float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
     float fl = -1.f;
 #pragma unroll
-    for (int i = 0; i < kGenLags; ++i) {
-        const int t = t0 + threadIdx.x + i * kGenThreads;
+    for (int i = 0; i < kLags; ++i) {
+        const int t = t0 + threadIdx.x + i * T;
         if (t < t1) {
             int d = abs(t - bidx);
             d = min(d, a.P - d);
-            if (d > a.radius) fl = fmaxf(fl, acc[i * kGenThreads]);  // acquisition.py:155-159
-            if (pm) pm[t] = acc[i * kGenThreads];
+            if (d > a.radius) fl = fmaxf(fl, acc[i * T]);  // acquisition.py:155-159
+            if (pm) pm[t] = acc[i * T];
         }
     }
 #pragma unroll
