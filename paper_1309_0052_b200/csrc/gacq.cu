@@ -119,6 +119,9 @@ void gen_passes(GenPlan& g) {
     for (int i = 0; i < n16; ++i) g.radix[g.n_pass++] = 16;
     if (rem == 5) { g.radix[g.n_pass++] = 8; g.radix[g.n_pass++] = 4; }
     else if (rem) g.radix[g.n_pass++] = (signed char)(1 << rem);
+    // fives in pairs as radix-25 passes (5 x 5 in registers: one pass and barrier pair less)
+    // when a thread holds 32 values per pass (T = 256)
+    for (; g.T == 256 && m % 25 == 0; m /= 25) g.radix[g.n_pass++] = 25;
     for (; m % 5 == 0; m /= 5) g.radix[g.n_pass++] = 5;
     for (; m % 3 == 0; m /= 3) g.radix[g.n_pass++] = 3;
 }
@@ -137,8 +140,8 @@ bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
                 g.M = (int)n_coh;
                 g.L = L;
                 g.Ms = (int)Ms;
-                gen_passes(g);
                 gen_threads(g);
+                gen_passes(g);
                 return true;
             }
         }
@@ -150,8 +153,8 @@ bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
     g.M = (int)M;
     g.L = (int)std::max<int64_t>(1, M / gacq::kGenMaxMs);
     g.Ms = (int)(M / g.L);
-    gen_passes(g);
     gen_threads(g);
+    gen_passes(g);
     return true;
 }
 

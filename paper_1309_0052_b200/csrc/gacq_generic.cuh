@@ -63,9 +63,39 @@ __device__ __forceinline__ cx gen_tw(const float2* __restrict__ tw, int e) {
     return pk(t.x, S < 0 ? -t.y : t.y);
 }
 
+// 25-point DFT as 5 x 5 (n = 5 n1 + n2, k = k1 + 5 k2): five 5-point DFTs over n1, the
+// twiddles W_25^(S n2 k1) as constants, five 5-point DFTs over n2; natural order in and out
+template <int S>
+__device__ __forceinline__ void dft25(cx (&v)[25]) {
+#pragma unroll
+    for (int n2 = 0; n2 < 5; ++n2) r_dft5<S>(v[n2], v[5 + n2], v[10 + n2], v[15 + n2], v[20 + n2]);
+    // v[5 k1 + n2] now holds Y[n2][k1]
+    // (cos, sin)(2 pi n2 k1 / 25), float32-rounded, at [(k1 - 1) 4 + n2 - 1]
+    constexpr float kC[16] = {0.9685831665992737f, 0.8763066530227661f, 0.728968620300293f, 0.5358268022537231f, 0.8763066530227661f, 0.5358268022537231f, 0.06279052048921585f, -0.4257792830467224f, 0.728968620300293f, 0.06279052048921585f, -0.6374239921569824f, -0.9921147227287292f, 0.5358268022537231f, -0.4257792830467224f, -0.9921147227287292f, -0.6374239921569824f};
+    constexpr float kS[16] = {0.24868988990783691f, 0.4817536771297455f, 0.6845471262931824f, 0.8443279266357422f, 0.4817536771297455f, 0.8443279266357422f, 0.9980267286300659f, 0.9048270583152771f, 0.6845471262931824f, 0.9980267286300659f, 0.7705132365226746f, 0.12533323466777802f, 0.8443279266357422f, 0.9048270583152771f, 0.12533323466777802f, -0.7705132365226746f};
+#pragma unroll
+    for (int k1 = 1; k1 < 5; ++k1)
+#pragma unroll
+        for (int n2 = 1; n2 < 5; ++n2) {
+            const int t = (k1 - 1) * 4 + n2 - 1;
+            v[5 * k1 + n2] = cmul(v[5 * k1 + n2], pk(kC[t], S < 0 ? -kS[t] : kS[t]));
+        }
+    cx o[25];
+#pragma unroll
+    for (int k1 = 0; k1 < 5; ++k1) {
+        r_dft5<S>(v[5 * k1], v[5 * k1 + 1], v[5 * k1 + 2], v[5 * k1 + 3], v[5 * k1 + 4]);
+#pragma unroll
+        for (int k2 = 0; k2 < 5; ++k2) o[k1 + 5 * k2] = v[5 * k1 + k2];
+    }
+#pragma unroll
+    for (int i = 0; i < 25; ++i) v[i] = o[i];
+}
+
 template <int S, int R>
 __device__ __forceinline__ void gen_dft(cx (&v)[R]) {
-    if constexpr (R == 16) {
+    if constexpr (R == 25) {
+        dft25<S>(v);
+    } else if constexpr (R == 16) {
         dft16<S>(v);
     } else if constexpr (R == 8) {
         dft8<S>(v);
@@ -119,6 +149,26 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
                 // W^r from the table powers W^1, W^2, W^4, W^8 and at most two products each
                 // (<= 3 roundings per twiddle): 4 loads instead of R - 1
                 cx w[R];
+                if constexpr (R == 25) {
+                    // W^(5a + b) = W^(5a) W^b from the loaded 1, 2, 4, 5, 10, 20 (<= 3 roundings)
+                    w[1] = gen_tw<S>(tw, e1);
+                    w[2] = gen_tw<S>(tw, 2 * e1);
+                    w[4] = gen_tw<S>(tw, 4 * e1);
+                    w[5] = gen_tw<S>(tw, 5 * e1);
+                    w[10] = gen_tw<S>(tw, 10 * e1);
+                    w[20] = gen_tw<S>(tw, 20 * e1);
+                    w[3] = cmul(w[1], w[2]);
+                    w[15] = cmul(w[5], w[10]);
+#pragma unroll
+                    for (int a5 = 5; a5 < 25; a5 += 5)
+#pragma unroll
+                        for (int b = 1; b < 5; ++b)
+                            if (a5 + b != 5 && a5 + b != 10 && a5 + b != 20) w[a5 + b] = cmul(w[a5], w[b]);
+#pragma unroll
+                    for (int r = 1; r < R; ++r) v[g][r] = cmul(v[g][r], w[r]);
+                    gen_dft<S, R>(v[g]);
+                    continue;
+                }
                 w[1] = gen_tw<S>(tw, e1);
                 if (R > 2) w[2] = gen_tw<S>(tw, 2 * e1);
                 if (R > 4 && R != 5) w[4] = gen_tw<S>(tw, 4 * e1);
@@ -240,8 +290,12 @@ struct GenArgs {
 };
 
 // 4-bit codes of the pass radices in GenArgs.sched
-__host__ __device__ constexpr int gen_radix_code(int R) { return R == 16 ? 6 : R == 8 ? 5 : R == 5 ? 4 : R == 4 ? 3 : R == 3 ? 2 : 1; }
-__host__ __device__ constexpr int gen_code_radix(int c) { return c == 6 ? 16 : c == 5 ? 8 : c == 4 ? 5 : c == 3 ? 4 : c == 2 ? 3 : 2; }
+__host__ __device__ constexpr int gen_radix_code(int R) {
+    return R == 25 ? 7 : R == 16 ? 6 : R == 8 ? 5 : R == 5 ? 4 : R == 4 ? 3 : R == 3 ? 2 : 1;
+}
+__host__ __device__ constexpr int gen_code_radix(int c) {
+    return c == 7 ? 25 : c == 6 ? 16 : c == 5 ? 8 : c == 4 ? 5 : c == 3 ? 4 : c == 2 ? 3 : 2;
+}
 
 // Every pass as an out-of-line function: each gets its own register allocation (inlined into
 // the runtime radix switch, the kernels spilled the values a pass holds across its barrier)
@@ -265,6 +319,9 @@ __device__ __forceinline__ void gen_fft_from(cx* __restrict__ x, const GenArgs& 
     for (int p = p0; p < a.n_pass; ++p) {
         const int R = gen_code_radix((int)((a.sched >> (4 * p)) & 15));
         switch (R) {
+            case 25:
+                if constexpr (VPT >= 25) gen_pass_call<S, 25, VPT>(x, Ms, Ns, tw);  // planned only when VPT >= 25
+                break;
             case 16: gen_pass_call<S, 16, VPT>(x, Ms, Ns, tw); break;
             case 8: gen_pass_call<S, 8, VPT>(x, Ms, Ns, tw); break;
             case 5: gen_pass_call<S, 5, VPT>(x, Ms, Ns, tw); break;
