@@ -135,6 +135,7 @@ bool gen_plan(int64_t n_coh, int64_t P, GenPlan& g) {
             if (n_coh % L) break;
             const int64_t Ms = n_coh / L;
             const bool pow2 = (Ms & (Ms - 1)) == 0;
+            // (splitting 8192 into a 2-CTA cluster of 4096-point, 256-thread CTAs measured 1.5x slower)
             if (Ms <= (pow2 ? gacq::kGenMaxMs : gacq::kGenMaxMsOdd)) {
                 g.native = true;
                 g.M = (int)n_coh;
