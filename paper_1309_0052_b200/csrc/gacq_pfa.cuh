@@ -296,7 +296,8 @@ struct CorrPfaArgs {
     unsigned long long* counter;  // zeroed before the launch
     int B, R, D, P, n_prn, radius;
     int zero;              // 0 (an opaque runtime zero, see dft31_stream)
-    unsigned dmagic;       // ceil(2^32 / D): x / D == umulhi(x, dmagic) for x < 2^32 / D
+    unsigned dmagic;       // ceil(2^32 / D) for D > 1: x / D == umulhi(x, dmagic) for x < 2^32 / D
+                           // (D = 1 has no 32-bit magic: divD returns x itself)
 };
 
 // chip lag of cell (q1, q2)
@@ -351,6 +352,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     }
     const unsigned n_prn = (unsigned)a.n_prn;
     const int D = a.D, R = a.R;
+    auto divD = [&](unsigned x) { return D == 1 ? x : __umulhi(x, a.dmagic); };  // x / D
     int unit = blockIdx.x;
     if (unit >= a.n_units) return;
     const int64_t pair_span = (int64_t)R * D * kSpec;
@@ -511,7 +513,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                     for (int rho = 0; rho < D; ++rho) {
                         const unsigned off = (unsigned)(D * kChips), uD = (unsigned)D;
                         const unsigned lo = (unsigned)(peak - a.radius - rho) + off, hi = (unsigned)(peak + a.radius - rho) + off;
-                        const int qa = (int)__umulhi(lo + uD - 1u, a.dmagic) - kChips, qb = (int)__umulhi(hi, a.dmagic) - kChips;
+                        const int qa = (int)divD(lo + uD - 1u) - kChips, qb = (int)divD(hi) - kChips;
                         const float* row = rows + rho * kTop2Row + lane;
                         const float v1 = row[0], v2 = row[32], c0 = row[96], c1 = row[128];
                         const int i1 = __float_as_int(row[64]);
@@ -533,7 +535,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                     // D * 1023 (> r + rho) so both bounds divide as unsigned
                     const unsigned off = (unsigned)(D * kChips), uD = (unsigned)D;
                     const unsigned lo = (unsigned)(peak - a.radius - rho) + off, hi = (unsigned)(peak + a.radius - rho) + off;
-                    const int qa = (int)__umulhi(lo + uD - 1u, a.dmagic) - kChips, qb = (int)__umulhi(hi, a.dmagic) - kChips;
+                    const int qa = (int)divD(lo + uD - 1u) - kChips, qb = (int)divD(hi) - kChips;
                     unsigned m31 = 0u, mx = 0u;
                     for (int q = qa; q <= qb; ++q) {
                         const int qq = q < 0 ? q + kChips : q >= kChips ? q - kChips : q;
