@@ -8,6 +8,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
+import oracle
 from golden_cases import case, if_bytes, if_decoded, load_cases
 from parity import compare
 
@@ -98,3 +99,23 @@ def test_quantized_misaligned_device_and_generic_path(pkg, name):
     gen = pkg.AcqEngine(fs, c["prns"], pkg.AcqConfig(**c["config"]), force_generic=True)
     np.testing.assert_array_equal(gen.run_rows_quantized(ints, fmt, scale), gen.run_rows(samples))
     gen.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_quantized_random_scales_equal_host_dequantized(pkg, seed):
+    # random full-scale values (1e-3 .. 1e4) and both integer formats: K1's in-register
+    # dequantization (int8 via its shared-memory table, int16 by DMUL) gives exactly the rows of
+    # the host-side float32(float64(q) * scale / limit) samples (iffile.py:95-98)
+    rng = np.random.default_rng(700 + seed)
+    fs = [4.092e6, 8.184e6, 2.046e6][seed % 3]
+    fmt = seed % 2  # 0: int8, 1: int16
+    limit = 127.0 if fmt == 0 else 32767.0
+    scale = float(10.0 ** rng.uniform(-3, 4))
+    cfg = pkg.AcqConfig(doppler_min_hz=-2000.0, doppler_max_hz=2000.0, doppler_step_hz=500.0, noncoherent_rounds=2)
+    x, _ = oracle.make_snapshot(seed, fs, 2e-3, base_seed=4400)
+    iq = np.stack([x.real, x.imag], -1).reshape(1, -1) / np.abs(x).max() * limit * 0.9
+    q = np.clip(np.round(iq), -limit, limit).astype(np.int8 if fmt == 0 else np.int16)
+    host = (q.astype(np.float64) * (scale / limit)).astype(np.float32).reshape(1, -1, 2)
+    samples = (host[..., 0] + 1j * host[..., 1]).astype(np.complex64)
+    eng = pkg.get_engine(fs, list(range(1, 33)), cfg)
+    np.testing.assert_array_equal(eng.run_rows_quantized(q, fmt, scale), eng.run_rows(samples))
