@@ -72,3 +72,40 @@ def test_random_config_matches_oracle(pkg, i):
             v = compare(gd, r, kw["detection_threshold"], pm, bins)
         assert v == "exact", (fs, kw, prn, v, eng.info)
     eng.close()
+
+
+@pytest.mark.parametrize("i", range(10))
+def test_random_batches_chunks_and_prn_sets(pkg, i):
+    # random batch sizes, PRN subsets (any order and count), strides and small spectrum scratch
+    # (many chunks, partial 4-pair groups in K2, short first chunk): every batch row equals the
+    # same snapshot searched alone, and the first snapshot equals the oracle
+    rng = np.random.default_rng(3300 + i)
+    fs = [4.092e6, 8.184e6, 5.0e6, 2.046e6, 6.0e6][i % 5]
+    kw = dict(doppler_min_hz=-1500.0, doppler_max_hz=1500.0, doppler_step_hz=500.0,
+              noncoherent_rounds=int(rng.integers(1, 3)))
+    prns = [int(p) for p in rng.permutation(np.arange(1, 33))[:int(rng.integers(1, 33))]]
+    n_snap = int(rng.integers(1, 14))
+    span = round(fs * 1e-3) * kw["noncoherent_rounds"]
+    pad = int(rng.integers(0, 9))
+    xs = np.zeros((n_snap, span + pad), dtype=np.complex64)
+    for s in range(n_snap):
+        xs[s, :span] = oracle.make_snapshot(s, fs, span / fs, base_seed=6100 + i)[0]
+    scratch = int(rng.integers(1, 6)) << 20  # 1-5 MiB: a few pairs per chunk
+    eng = pkg.AcqEngine(fs, prns, pkg.AcqConfig(**kw), scratch_bytes=scratch)
+    rows = eng.run_rows(xs)
+    one = pkg.AcqEngine(fs, prns, pkg.AcqConfig(**kw))
+    for s in range(n_snap):
+        np.testing.assert_array_equal(rows[s], one.run_rows(np.ascontiguousarray(xs[s:s + 1, :span]))[0])
+    ocfg = oracle.OracleConfig(**kw)
+    bins = ocfg.doppler_bins_hz()
+    for g, prn in zip(eng.search(xs[:1]).results()[0], prns):
+        r = oracle.acquire_channel(xs[0, :span], fs, prn, ocfg)
+        gd = dict(doppler_hz=g.doppler_hz, code_phase_samples=g.code_phase_samples, peak_metric=g.peak_metric,
+                  detected=g.detected)
+        v = compare(gd, r, ocfg.detection_threshold)
+        if v != "exact":
+            v = compare(gd, r, ocfg.detection_threshold,
+                        oracle.acquire_channel(xs[0, :span], fs, prn, ocfg, want_map=True)["power_map"], bins)
+        assert v == "exact", (fs, prn, v)
+    eng.close()
+    one.close()
