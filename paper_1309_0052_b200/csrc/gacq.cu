@@ -298,10 +298,13 @@ cudaError_t launch_fwd_pfa(const gacq_ctx* c, const FwdPfaArgs& fa, int64_t bloc
 cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_units);
     // phase summaries when every exclusion window spans <= 33 chip lags (gacq_pfa.cuh, kTop2)
-    if (2 * (int64_t)ca.radius < 33 * (int64_t)ca.D)
-        gacq_corr_pfa_kernel<true><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
+    const bool top2 = 2 * (int64_t)ca.radius < 33 * (int64_t)ca.D;
+    if (top2 && ca.R == 1)
+        gacq_corr_pfa_kernel<true, true><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
+    else if (top2)
+        gacq_corr_pfa_kernel<true, false><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
     else
-        gacq_corr_pfa_kernel<false><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
+        gacq_corr_pfa_kernel<false, false><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
     return cudaGetLastError();
 }
 
@@ -769,7 +772,8 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     }
     {
         // every PFA variant gets the largest dynamic shared memory any plan launches it with
-        for (const void* k : {(const void*)gacq_corr_pfa_kernel<true>, (const void*)gacq_corr_pfa_kernel<false>}) {
+        for (const void* k : {(const void*)gacq_corr_pfa_kernel<true, false>, (const void*)gacq_corr_pfa_kernel<false, false>,
+                              (const void*)gacq_corr_pfa_kernel<true, true>}) {
             CTX_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, corr_pfa_smem()));
             CTX_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         }
@@ -780,11 +784,14 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
 #undef GACQ_ATTR_FWDP
         int per_sm = 0, sms = 0;
         int per_sm_full = 0;
-        CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<true>, 32 * kCorrWarps,
-                                                              corr_pfa_smem()));
-        CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_full, gacq_corr_pfa_kernel<false>,
+        int per_sm_r1 = 0;
+        CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gacq_corr_pfa_kernel<true, false>,
                                                               32 * kCorrWarps, corr_pfa_smem()));
-        per_sm = std::min(per_sm, per_sm_full);
+        CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_full, gacq_corr_pfa_kernel<false, false>,
+                                                              32 * kCorrWarps, corr_pfa_smem()));
+        CTX_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_r1, gacq_corr_pfa_kernel<true, true>,
+                                                              32 * kCorrWarps, corr_pfa_smem()));
+        per_sm = std::min({per_sm, per_sm_full, per_sm_r1});
         CTX_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
         c->corr_slots = std::max(1, per_sm) * (int64_t)sms;
         CTX_TRY(cudaMalloc(&c->d_prow, (size_t)c->corr_slots * kCorrWarps * c->D * kPhaseRow * sizeof(float)));

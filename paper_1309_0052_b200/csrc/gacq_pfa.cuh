@@ -337,7 +337,9 @@ __device__ __forceinline__ bool excluded(int lag, int peak, int P, int radius) {
 // its 31 per phase (its q values are congruent mod 33) and at most one of the spread row's, so a
 // phase keeps only the lane's (max, its first index, second max) and the two spread-row cells: 5
 // words per lane instead of the 33-float row, and the floor reads them back with no window loop.
-template <bool kTop2>
+// kR1 (one noncoherent round, C1): the phase summary is tracked inside the round's |g|^2 emit
+// (ALU work interleaved with the Rader stage's FMAs) instead of a pass over the 31 powers after it.
+template <bool kTop2, bool kR1>
 __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a) {
     __shared__ int s_unit[2];
     extern __shared__ __align__(16) cx smem[];
@@ -400,6 +402,8 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
 #pragma unroll
                 for (int i = 0; i < 31; ++i) acc[i] = 0.f;
                 accx[0] = accx[1] = 0.f;
+                float v1 = -1.f, v2 = -1.f;  // kTop2: the lane's first max, second max (ties twice), index
+                int i1 = 0;
 #pragma unroll 1
                 for (int rd = 0; rd < R; ++rd, ++t) {
                     // the warp's next spectrum: next round, else the next phase's first round, else
@@ -430,7 +434,16 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                     // scratch in E[1023..1055])
                     const cx e = lane < 31 ? E[32 * 31 + lane] : czero();
                     const cx* Er = E + lane * 31;
-                    dft31_rader_inv([&](int k1) { return Er[k1]; }, [&](int q1, cx v) { acc[q1] = pow_acc(v, acc[q1]); });
+                    dft31_rader_inv([&](int k1) { return Er[k1]; }, [&](int q1, cx v) {
+                        const float pw = pow_acc(v, acc[q1]);
+                        acc[q1] = pw;
+                        if constexpr (kTop2 && kR1) {  // first max in emission order
+                            const bool gt = pw > v1;
+                            v2 = gt ? v1 : fmaxf(v2, pw);
+                            i1 = gt ? q1 : i1;
+                            v1 = gt ? pw : v1;
+                        }
+                    });
                     coop31<1>(e, lane, [&](int j) { return __ldg(&kCoop31Coef[j - 1][lane]); }, E + kChips,
                               [&](int sl, int, cx v) { accx[sl] = pow_acc(v, accx[sl]); });
                     __syncwarp();  // E is free for the next transform
@@ -438,15 +451,15 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 // phase done: the row to scratch (and the parity power map), the running first argmax
                 float m;
                 if constexpr (kTop2) {
-                    float v1 = -1.f, v2 = -1.f;
-                    int i1 = 0;
+                    if constexpr (!kR1) {
 #pragma unroll
-                    for (int q1 = 0; q1 < 31; ++q1) {  // first max, and the second max (ties count twice)
-                        const float v = acc[q1];
-                        const bool gt = v > v1;
-                        v2 = gt ? v1 : fmaxf(v2, v);
-                        i1 = gt ? q1 : i1;
-                        v1 = gt ? v : v1;
+                        for (int q1 = 0; q1 < 31; ++q1) {  // first max, and the second max (ties count twice)
+                            const float v = acc[q1];
+                            const bool gt = v > v1;
+                            v2 = gt ? v1 : fmaxf(v2, v);
+                            i1 = gt ? q1 : i1;
+                            v1 = gt ? v : v1;
+                        }
                     }
                     float* row = rows + rho * kTop2Row + lane;
                     row[0] = v1;
@@ -476,13 +489,17 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                 m = fmaxf(m, fmaxf(accx[0], accx[1]));
                 if (m >= best) {
                     int bl = 0x7fffffff;
-                    unsigned mk = 0u;
+                    if (kTop2 && v1 == m && v2 < v1) {  // one main cell holds the lane max: its lag
+                        bl = D * cell_q(i1, lane) + rho;
+                    } else {  // ties (or a spread-row max): the lowest lag among the cells equal to it
+                        unsigned mk = 0u;
 #pragma unroll
-                    for (int q1 = 0; q1 < 31; ++q1) mk |= (acc[q1] == m ? 1u : 0u) << q1;
-                    while (mk) {
-                        const int q1 = __ffs(mk) - 1;
-                        mk &= mk - 1u;
-                        bl = min(bl, D * cell_q(q1, lane) + rho);
+                        for (int q1 = 0; q1 < 31; ++q1) mk |= (acc[q1] == m ? 1u : 0u) << q1;
+                        while (mk) {
+                            const int q1 = __ffs(mk) - 1;
+                            mk &= mk - 1u;
+                            bl = min(bl, D * cell_q(q1, lane) + rho);
+                        }
                     }
                     if (x0 && accx[0] == m) bl = min(bl, D * cell_q(lane == 16 ? 0 : lane, 32) + rho);
                     if (x1 && accx[1] == m) bl = min(bl, D * cell_q(31 - lane, 32) + rho);
