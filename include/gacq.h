@@ -61,7 +61,8 @@ typedef struct gacq_params {
     const int32_t* prns;              /* PRN numbers 1..32, distinct                      */
     int32_t device;                   /* CUDA ordinal                                     */
     int32_t plan_flags;               /* GACQ_PLAN_* (0 = default)                        */
-    int64_t scratch_bytes;            /* spectrum scratch budget, 0 = default (1 GiB)     */
+    int64_t scratch_bytes;            /* spectrum scratch budget, 0 = default: min(8 GiB,  */
+                                      /* free device memory / 4); allocated on demand      */
 } gacq_params;
 
 /* One reduced search row: the winning (bin, lag) of a (snapshot, prn) -- or of a

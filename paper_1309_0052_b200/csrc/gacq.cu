@@ -224,8 +224,10 @@ struct gacq_ctx {
     std::vector<int32_t> prns;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     float2* d_carrier = nullptr;
-    cx* d_Z = nullptr;
-    int64_t z_pairs = 0;  // pairs per chunk that fit in the scratch
+    char* d_Z = nullptr;
+    int64_t z_pairs = 0;     // pairs per chunk that fit in the scratch budget
+    int64_t z_bytes = 0;     // allocated scratch (grown on demand, up to the budget)
+    int64_t pair_bytes = 0;  // spectra of one (snapshot, bin) pair
     float2* d_in = nullptr;
     int64_t in_cap = 0;   // complex64 staging (samples)
     char* d_raw = nullptr;
@@ -449,6 +451,11 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (!inp.on_device) c->stats.h2d_bytes += n_snap * span * sb;
     }
     const bool on_device = !staged;
+    {   // spectrum scratch: the largest chunk this call runs (whole K2 pair groups)
+        int64_t need = std::min(c->z_pairs, n_pairs);
+        if (!c->gen) need = std::min(c->z_pairs, (need + kCorrWarps - 1) / kCorrWarps * kCorrWarps);
+        if ((rc = grow(&c->d_Z, &c->z_bytes, need * c->pair_bytes))) return rc;
+    }
 
     size_t ev = 2;
     int64_t waited = -1;
@@ -468,7 +475,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
                 CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[k], 0));
             waited = std::max(waited, need);
         }
-        cx* Zp = reinterpret_cast<cx*>(c->d_Z);
+        cx* Zp = reinterpret_cast<cx*>(c->d_Z);  // (char-typed allocation, 16-byte aligned by cudaMalloc)
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
         GenArgs ga{(const float2*)in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
                    pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->n_prn, c->radius, c->gp.M, c->gp.Ms,
@@ -760,10 +767,16 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
     }
     const int64_t pair_bytes = (int64_t)c->R * (gen ? (int64_t)gp.M : (int64_t)c->D * kSpec) *
                                (int64_t)sizeof(float2);
-    const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes : (int64_t)1 << 30;
+    c->pair_bytes = pair_bytes;
+    // default budget: 8 GiB (C3's 1024-snapshot batch, 7.3 GB of spectra, in one chunk: no
+    // persistent-grid tails between chunks, +1.2% over 1 GiB), at most a quarter of the free
+    // device memory; allocated on demand by run_impl, so small batches hold little
+    size_t free_b = 0, total_b = 0;
+    CTX_TRY(cudaMemGetInfo(&free_b, &total_b));
+    const int64_t budget = p->scratch_bytes > 0 ? p->scratch_bytes
+                                                : std::min<int64_t>((int64_t)8 << 30, (int64_t)(free_b / 4));
     c->z_pairs = std::max<int64_t>(1, budget / pair_bytes);
     if (!gen && c->z_pairs > kCorrWarps) c->z_pairs -= c->z_pairs % kCorrWarps;  // whole K2 pair groups per chunk
-    CTX_TRY(cudaMalloc(&c->d_Z, c->z_pairs * pair_bytes));
     CTX_TRY(cudaMalloc(&c->d_bad, sizeof(int)));
     CTX_TRY(cudaHostAlloc(&c->h_bad, sizeof(int), cudaHostAllocPortable));
     if (gen) {
