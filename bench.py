@@ -535,9 +535,10 @@ def run_ours(args, rank, world, local_rank):
         rates, cpu_results, call_s, sample = cpu_measure(args.config, list(host), reps, 0, cores)
         cpu_baseline = {"value": statistics.mean(rates), "unit": UNIT, "cores": cores, "kind": "port",
                         "sample": sample, "single_call_ms": call_s * 1e3,
-                        "port_vs_reference": "the port runs 1.30x faster per process than gnssperf.acquire_all "
-                                             "on the same C3 snapshot (0.84 s vs 1.09 s, measured in the build "
-                                             "container, DESIGN.md section 8): ratios against it are conservative"}
+                        "port_vs_reference": "the port runs 1.15-1.36x faster per process than gnssperf.acquire_all "
+                                             "on the same C3 snapshot (0.57-0.77 s vs 0.69-1.04 s, identical results, "
+                                             "measured in the build container, DESIGN.md section 8): ratios against "
+                                             "it are conservative"}
     barrier()
 
     # ---- value: strong scaling of the fixed global batch
