@@ -15,6 +15,7 @@ from .acquisition import (  # noqa: F401
     acquire_bins_sharded,
     acquire_channel,
     acquire_if_file,
+    conjugate_code_spectrum,
     default_doppler_step_hz,
     get_engine,
     merge_bin_shards,

@@ -86,6 +86,46 @@ def samples_per_code_period(sample_rate_hz: float) -> int:
     return round(sample_rate_hz * CODE_LENGTH / CHIP_RATE_HZ)
 
 
+_code_spectrum_cache: dict = {}
+_cache_lock = threading.Lock()
+_CODE_SCALE = 1 << 42  # kernels.py:51-53: 42-bit code NCO fraction
+_CODE_MODULUS = CODE_LENGTH * _CODE_SCALE
+
+
+def conjugate_code_spectrum(prn: int, sample_rate_hz: float, n: int, precision: Precision = Precision.SINGLE):
+    """Drop-in for gnssperf.acquisition.conjugate_code_spectrum (acquisition.py:88-105):
+    conj(FFT_n(code replica)) of one PRN, cached immutably per (prn, fs, n, precision).
+
+    The replica is the reference's floor-indexed code NCO from phase 0
+    (gnss_signal.py:75-96, kernels.py:65-70: chip index ((k * step) mod 1023*2^42) >> 42), in the
+    precision's complex dtype, transformed with scipy.fft as the reference's dsp backend does
+    (dsp.py:82-85), so the bins are the reference's bit for bit. This is a host helper for
+    callers that use the reference's API directly; the GPU search never calls it (gacq_create
+    builds its own code spectra on the device)."""
+    key = (int(prn), float(sample_rate_hz), int(n), precision)
+    spec = _code_spectrum_cache.get(key)
+    if spec is not None:
+        return spec
+    if n < 1:
+        raise InvalidInputError("sample_code_replica needs n >= 1")
+    if sample_rate_hz <= 0:
+        raise InvalidInputError("rates must be > 0")
+    with _cache_lock:
+        spec = _code_spectrum_cache.get(key)
+        if spec is None:
+            from scipy import fft as _sfft  # the reference's FFT dependency (host helper only)
+
+            chips = generate_ca_code(int(prn)).chips
+            step = int(round((CHIP_RATE_HZ / sample_rate_hz) * _CODE_SCALE))  # kernels.py:69-70
+            k = np.arange(int(n), dtype=object)
+            idx = np.array([((int(v) * step) % _CODE_MODULUS) >> 42 for v in k], dtype=np.int64)
+            replica = chips[idx].astype(precision.complex_dtype)
+            spec = np.conj(_sfft.fft(replica))
+            spec.setflags(write=False)
+            _code_spectrum_cache[key] = spec
+    return spec
+
+
 @dataclass
 class BatchResult:
     """Vectorised results of a batch: every array is [n_snap, n_prn]."""

@@ -129,3 +129,42 @@ def test_finish_metric_semantics(pkg):
     assert r[0] == pkg.AcqResult(3, 500.0, 17, 2.5, True, 3, 123)
     assert r[1].peak_metric == float("inf") and r[1].detected
     eng._ctx = None
+
+
+@pytest.mark.parametrize("fs,n", [(4.092e6, 4092), (8.184e6, 16368), (5.0e6, 5000), (2.046e6, 2046)])
+def test_conjugate_code_spectrum_drop_in(pkg, fs, n):
+    # acquisition.py:88-105: same bins as the pinned oracle (which restates the reference bit for
+    # bit), complex64 for SINGLE, read-only and cached; DOUBLE gives the complex128 spectrum
+    got = pkg.conjugate_code_spectrum(7, fs, n, pkg.Precision.SINGLE)
+    from oracle import gnss_oracle
+
+    want = gnss_oracle.conjugate_code_spectrum(7, fs, n)
+    assert got.dtype == np.complex64 and not got.flags.writeable
+    np.testing.assert_array_equal(got, want)
+    assert pkg.conjugate_code_spectrum(7, fs, n, pkg.Precision.SINGLE) is got
+    dbl = pkg.conjugate_code_spectrum(7, fs, n, pkg.Precision.DOUBLE)
+    assert dbl.dtype == np.complex128
+    np.testing.assert_allclose(dbl, want.astype(np.complex128), rtol=0, atol=1e-3)
+
+
+def test_conjugate_code_spectrum_equals_reference_itself(pkg):
+    # in the build container the reference package is importable: compare with its own function
+    import sys
+    from pathlib import Path
+
+    src = Path("/root/reference/pkg/src")
+    if not src.exists():
+        pytest.skip("reference sources not present (GPU box)")
+    sys.path.insert(0, str(src))
+    try:
+        from gnssperf import acquisition as ref_acq
+        from gnssperf.buffers import Precision as RefPrecision
+    except Exception as exc:  # noqa: BLE001 - optional dependency chain
+        pytest.skip(f"reference not importable: {exc}")
+    finally:
+        sys.path.remove(str(src))
+    for fs, n, prn in ((4.092e6, 4092, 3), (8.184e6, 8184, 31), (5.0e6, 10000, 12)):
+        np.testing.assert_array_equal(pkg.conjugate_code_spectrum(prn, fs, n, pkg.Precision.SINGLE),
+                                      ref_acq.conjugate_code_spectrum(prn, fs, n, RefPrecision.SINGLE))
+        np.testing.assert_array_equal(pkg.conjugate_code_spectrum(prn, fs, n, pkg.Precision.DOUBLE),
+                                      ref_acq.conjugate_code_spectrum(prn, fs, n, RefPrecision.DOUBLE))
