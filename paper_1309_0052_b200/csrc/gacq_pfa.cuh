@@ -49,7 +49,7 @@ __host__ __device__ constexpr int fwd_pfa_main(int D, int W) {
 __host__ __device__ constexpr int fwd_pfa_smem(int D, int W) { return fwd_pfa_main(D, W) + 256 * 4; }
 
 // ---- bulk async copy + mbarrier (SASS UBLKCP / SYNCS) ------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -83,9 +83,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
+
 
 __device__ __forceinline__ float pow_acc(cx v, float acc) { return fmaf(im(v), im(v), fmaf(re(v), re(v), acc)); }
 
