@@ -386,6 +386,9 @@ cudaError_t launch_dequant(const gacq_ctx* c, const Input& in, int64_t s0, int64
 }
 
 // Core pipeline. `in.ptr` is a device pointer when in.on_device, else a host pointer.
+#ifndef GACQ_CHUNK_GROWTH
+#define GACQ_CHUNK_GROWTH 8  // staged input: each compute chunk this many times the previous (4: e2e -0.6% C3, -1.5% C1)
+#endif
 int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool profile, gacq_row* rows_out,
              bool rows_on_device, float* pmap) {
     const int64_t span = (int64_t)c->R * c->n_coh;
@@ -461,13 +464,13 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
     int64_t waited = -1;
     std::vector<std::pair<size_t, int>> timed;  // (event index, kernel kind)
     // staged input: a short first chunk (its snapshots arrive first) hides the pipeline fill, and
-    // the chunks then grow 4x up to z_pairs, so each one waits only for the snapshots it reads
+    // the chunks then grow 8x up to z_pairs, so each one waits only for the snapshots it reads
     // while the copy stream stays ahead (H2D of a snapshot is ~10x faster than its search)
     int64_t want = !on_device ? std::min(c->z_pairs, std::max<int64_t>(copy_chunk * c->B, 2 * c->corr_slots / std::max(1, c->n_prn) + 1))
                               : c->z_pairs;
     for (int64_t p0 = 0, np = 0; p0 < n_pairs; p0 += np) {
         np = std::min(want, n_pairs - p0);
-        want = std::min(c->z_pairs, 4 * want);
+        want = std::min(c->z_pairs, GACQ_CHUNK_GROWTH * want);
         if (!on_device) {
             const int64_t last_snap = (p0 + np - 1) / c->B;
             const int64_t need = last_snap / copy_chunk;
