@@ -117,8 +117,11 @@ def conjugate_code_spectrum(prn: int, sample_rate_hz: float, n: int, precision: 
 
             chips = generate_ca_code(int(prn)).chips
             step = int(round((CHIP_RATE_HZ / sample_rate_hz) * _CODE_SCALE))  # kernels.py:69-70
-            k = np.arange(int(n), dtype=object)
-            idx = np.array([((int(v) * step) % _CODE_MODULUS) >> 42 for v in k], dtype=np.int64)
+            # k * step < 2^20 * 2^42 for any n < 2^20 samples: exact in uint64
+            if n >= 1 << 20:
+                raise InvalidInputError("conjugate_code_spectrum: n must be < 2^20 samples")
+            k = np.arange(int(n), dtype=np.uint64)
+            idx = (((k * np.uint64(step)) % np.uint64(_CODE_MODULUS)) >> np.uint64(42)).astype(np.int64)
             replica = chips[idx].astype(precision.complex_dtype)
             spec = np.conj(_sfft.fft(replica))
             spec.setflags(write=False)
