@@ -362,11 +362,16 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         for (int i = threadIdx.x; i < kCcHalf / 2; i += blockDim.x) cp_async16(dst + 2 * i, g + 16 * i);
         cp_async_commit();
     };
-    auto pair_of = [&](int u) { return (int)((unsigned)u / n_prn) * kCorrWarps + w; };  // this warp's pair
+    // R = 1: a unit spans kIPW pairs per warp (one unit barrier and code-spectrum swap per two
+    // items: at one transform per phase the per-unit work is a large share of the item)
+    constexpr int kIPW = kR1 ? 2 : 1;
+    auto pair_of = [&](int u, int it) {  // this warp's it-th pair of unit u
+        return (int)((unsigned)u / n_prn) * (kCorrWarps * kIPW) + it * kCorrWarps + w;
+    };
     if (threadIdx.x == 0) s_unit[1] = (int)(gridDim.x + atomicAdd(a.counter, 1ull));
     load_cc(unit, 0);
     {
-        const int lp = pair_of(unit);
+        const int lp = pair_of(unit, 0);
         __syncwarp();
         if (lane == 0 && lp < a.n_pairs) bulk_load(zbuf, a.Z + lp * pair_span, kSpecBytes, mbar);
     }
@@ -382,8 +387,12 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
         if (nxt < a.n_units) load_cc(nxt, (k + 1) & 1);  // its slot was last read in unit k - 1
         if (threadIdx.x == 0) s_unit[k & 1] = nxt < a.n_units ? (int)(gridDim.x + atomicAdd(a.counter, 1ull)) : a.n_units;
         const cx* ccs = ccs0 + (k & 1) * kCcHalf;
-        const int lp = pair_of(unit), pi = (int)((unsigned)unit % n_prn);
-        const int lpn = nxt < a.n_units ? pair_of(nxt) : a.n_pairs;  // the warp's next item
+        const int pi = (int)((unsigned)unit % n_prn);
+#pragma unroll 1
+        for (int it = 0; it < kIPW; ++it) {
+        const int lp = pair_of(unit, it);
+        // the warp's next item: its next pair in this unit, else its first pair of the next unit
+        const int lpn = it + 1 < kIPW ? pair_of(unit, it + 1) : nxt < a.n_units ? pair_of(nxt, 0) : a.n_pairs;
         const cx* znext = lpn < a.n_pairs ? a.Z + lpn * pair_span : nullptr;
         if (lp < a.n_pairs) {
             const cx* zb = a.Z + lp * pair_span;
@@ -598,6 +607,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
             __syncwarp();
             if (lane == 0) bulk_load_nofence(zbuf, znext, kSpecBytes, mbar);
         }
+        }  // items of the unit
         cp_async_wait_all();
         __syncthreads();  // the next unit's code spectrum and claim are visible; this unit's slot is free
         unit = nxt;
