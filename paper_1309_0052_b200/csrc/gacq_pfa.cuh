@@ -364,7 +364,10 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     };
     // R = 1: a unit spans kIPW pairs per warp (one unit barrier and code-spectrum swap per two
     // items: at one transform per phase the per-unit work is a large share of the item)
-    constexpr int kIPW = kR1 ? 2 : 1;
+#ifndef GACQ_R1_IPW
+#define GACQ_R1_IPW 2
+#endif
+    constexpr int kIPW = kR1 ? GACQ_R1_IPW : 1;
     auto pair_of = [&](int u, int it) {  // this warp's it-th pair of unit u
         return (int)((unsigned)u / n_prn) * (kCorrWarps * kIPW) + it * kCorrWarps + w;
     };
