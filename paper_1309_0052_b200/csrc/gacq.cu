@@ -431,9 +431,20 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             c->copy_events.push_back(e);
         }
+        // the copies are enqueued lazily, a compute chunk ahead (enqueue_copies below), so the
+        // first compute chunk reaches the GPU after a few API calls rather than after all of them
+        if (!inp.on_device) c->stats.h2d_bytes += n_snap * span * sb;
+    }
+    const bool on_device = !staged;
+    int64_t copies_enqueued = 0;
+    // enqueue the copy chunks (H2D and/or dequantization on the copy stream) that cover
+    // snapshots [0, snap_end), each ending in copy_events[k]
+    auto enqueue_copies = [&](int64_t snap_end) -> int {
+        if (!staged) return GACQ_OK;
+        const int64_t sb = sample_bytes(inp.fmt);
         const char* src = (const char*)inp.ptr;
-        for (int64_t k = 0; k < n_copy_chunks; ++k) {
-            const int64_t s0 = k * copy_chunk, ns = std::min(copy_chunk, n_snap - s0);
+        for (; copies_enqueued < n_copy_chunks && copies_enqueued * copy_chunk < snap_end; ++copies_enqueued) {
+            const int64_t k = copies_enqueued, s0 = k * copy_chunk, ns = std::min(copy_chunk, n_snap - s0);
             if (!quantized) {
                 CUDA_TRY(cudaMemcpy2DAsync(c->d_in + s0 * span, span * sb, src + s0 * inp.stride * sb,
                                            inp.stride * sb, span * sb, ns, cudaMemcpyHostToDevice, c->copy_stream));
@@ -451,9 +462,8 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
             }
             CUDA_TRY(cudaEventRecord(c->copy_events[k], c->copy_stream));
         }
-        if (!inp.on_device) c->stats.h2d_bytes += n_snap * span * sb;
-    }
-    const bool on_device = !staged;
+        return GACQ_OK;
+    };
     {   // spectrum scratch: the largest chunk this call runs (whole K2 pair groups)
         int64_t need = std::min(c->z_pairs, n_pairs);
         if (!c->gen) need = std::min(c->z_pairs, (need + kCorrWarps - 1) / kCorrWarps * kCorrWarps);
@@ -473,6 +483,10 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         want = std::min(c->z_pairs, GACQ_CHUNK_GROWTH * want);
         if (!on_device) {
             const int64_t last_snap = (p0 + np - 1) / c->B;
+            // this chunk's copies and the next (GACQ_CHUNK_GROWTH x larger) chunk's, so the copy
+            // stream stays ahead while the host enqueues this chunk's kernels
+            const int64_t next_end = std::min(n_pairs, p0 + np + std::min(want, n_pairs - p0 - np));
+            if ((rc = enqueue_copies((next_end + c->B - 1) / c->B))) return rc;
             const int64_t need = last_snap / copy_chunk;
             for (int64_t k = waited + 1; k <= need; ++k)
                 CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[k], 0));
