@@ -513,7 +513,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         } else {
             // pairs per warp per unit: 2 in the R = 1 instantiation (gacq_pfa.cuh kIPW), which
             // launch_corr_pfa picks for one round with the phase-summary floor
-            const int ipw = (c->R == 1 && 2 * (int64_t)c->radius < 33 * (int64_t)c->D) ? GACQ_R1_IPW : 1;
+            const int ipw = (c->R == 1 && 2 * (int64_t)c->radius < 33 * (int64_t)c->D) ? kR1PairsPerWarp : 1;
             const int64_t n_units = (np + kCorrWarps * ipw - 1) / (kCorrWarps * ipw) * c->n_prn;
             if (n_units + c->corr_slots >= INT32_MAX) return fail(GACQ_ERR_UNSUPPORTED, "chunk too large");
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_prow, p0, (int)np,

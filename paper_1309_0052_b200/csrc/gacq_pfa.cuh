@@ -31,6 +31,10 @@ constexpr int kCcHalf = 17 * 31 + 1;             // Hermitian half [k2 <= 16][31
 constexpr int kCorrWarps = 4;                    // K2 warps per CTA (one item each)
 constexpr int kPhaseRow = 33 * 32;               // K2 scratch row of one phase: [q1 or coop slot][lane] floats
 constexpr int kTop2Row = 5 * 32;                 // K2 (kTop2) phase summary: [max, 2nd max, max index, coop 0, coop 1][lane]
+#ifndef GACQ_R1_IPW
+#define GACQ_R1_IPW 2
+#endif
+constexpr int kR1PairsPerWarp = GACQ_R1_IPW;     // K2 at R = 1: pairs per warp per unit (kIPW)
 #ifndef GACQ_PFA_MAXNREG
 #define GACQ_PFA_MAXNREG 168                     // 3 CTAs x 4 warps per SM; no spills (streamed stages)
 #endif
@@ -364,10 +368,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     };
     // R = 1: a unit spans kIPW pairs per warp (one unit barrier and code-spectrum swap per two
     // items: at one transform per phase the per-unit work is a large share of the item)
-#ifndef GACQ_R1_IPW
-#define GACQ_R1_IPW 2
-#endif
-    constexpr int kIPW = kR1 ? GACQ_R1_IPW : 1;
+    constexpr int kIPW = kR1 ? kR1PairsPerWarp : 1;
     auto pair_of = [&](int u, int it) {  // this warp's it-th pair of unit u
         return (int)((unsigned)u / n_prn) * (kCorrWarps * kIPW) + it * kCorrWarps + w;
     };
