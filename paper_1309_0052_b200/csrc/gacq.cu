@@ -297,11 +297,16 @@ cudaError_t launch_fwd_pfa(const gacq_ctx* c, const FwdPfaArgs& fa, int64_t bloc
     return cudaErrorInvalidConfiguration;
 }
 
+// K2 variant: phase summaries when every exclusion window spans <= 33 chip lags (kTop2), and the
+// R = 1 instantiation (kR1, kR1PairsPerWarp pairs per warp per unit) on top of that
+bool corr_pfa_top2(int radius, int D) { return 2 * (int64_t)radius < 33 * (int64_t)D; }
+bool corr_pfa_r1(int radius, int D, int R) { return R == 1 && corr_pfa_top2(radius, D); }
+
 cudaError_t launch_corr_pfa(const gacq_ctx* c, const CorrPfaArgs& ca) {
     const int64_t blocks = std::min<int64_t>(c->corr_slots, ca.n_units);
     // phase summaries when every exclusion window spans <= 33 chip lags (gacq_pfa.cuh, kTop2)
-    const bool top2 = 2 * (int64_t)ca.radius < 33 * (int64_t)ca.D;
-    if (top2 && ca.R == 1)
+    const bool top2 = corr_pfa_top2(ca.radius, ca.D);
+    if (corr_pfa_r1(ca.radius, ca.D, ca.R))
         gacq_corr_pfa_kernel<true, true><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
     else if (top2)
         gacq_corr_pfa_kernel<true, false><<<(unsigned)blocks, 32 * kCorrWarps, corr_pfa_smem(), c->stream>>>(ca);
@@ -511,9 +516,8 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (c->gen) {
             CUDA_TRY(launch_gen(c, ga, np, true));
         } else {
-            // pairs per warp per unit: 2 in the R = 1 instantiation (gacq_pfa.cuh kIPW), which
-            // launch_corr_pfa picks for one round with the phase-summary floor
-            const int ipw = (c->R == 1 && 2 * (int64_t)c->radius < 33 * (int64_t)c->D) ? kR1PairsPerWarp : 1;
+            // pairs per warp per unit: kR1PairsPerWarp in the R = 1 instantiation launch_corr_pfa picks
+            const int ipw = corr_pfa_r1(c->radius, c->D, c->R) ? kR1PairsPerWarp : 1;
             const int64_t n_units = (np + kCorrWarps * ipw - 1) / (kCorrWarps * ipw) * c->n_prn;
             if (n_units + c->corr_slots >= INT32_MAX) return fail(GACQ_ERR_UNSUPPORTED, "chunk too large");
             CorrPfaArgs ca{Zp, reinterpret_cast<const cx*>(c->d_ccp), c->d_rows_bin, pmap, c->d_prow, p0, (int)np,
