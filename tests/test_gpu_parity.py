@@ -358,9 +358,10 @@ RADIUS_CASES = [(4.092e6, r) for r in (1, 4, 10, 64, 65, 66, 67, 200, 2000, 2045
                [(8.184e6, r) for r in (8, 131, 132, 500)] + [(16.368e6, r) for r in (16, 263, 264)]
 
 
+@pytest.mark.parametrize("rounds", [2, 1])  # R = 1 also selects K2's kR1 instantiation (summaries)
 @pytest.mark.parametrize("fs,radius", RADIUS_CASES)
-def test_exclusion_radius_floor_forms(pkg, fs, radius):
-    kw = dict(doppler_min_hz=-2000.0, doppler_max_hz=2000.0, doppler_step_hz=500.0, noncoherent_rounds=2,
+def test_exclusion_radius_floor_forms(pkg, fs, radius, rounds):
+    kw = dict(doppler_min_hz=-2000.0, doppler_max_hz=2000.0, doppler_step_hz=500.0, noncoherent_rounds=rounds,
               exclusion_radius_samples=radius)
     ocfg = oracle.OracleConfig(**kw)
     bins = ocfg.doppler_bins_hz()
