@@ -93,11 +93,17 @@ struct GenPlan {
     int T = 512;  // threads per CTA: 256 (two CTAs per SM) when two CTAs' shared memory fits
     bool native = false;
     signed char radix[gacq::kGenMaxPasses] = {};
-    unsigned long long sched() const {
+    // warp split (gacq_gen_corr_ws_kernel): W = T / 32 transforms of Q = Ms / W points, W = 1 off
+    int W = 1, Q = 0, n_wpass = 0;
+    signed char wradix[gacq::kGenMaxPasses] = {};
+    static unsigned long long code(const signed char* r, int n) {
         unsigned long long v = 0;
-        for (int p = 0; p < n_pass; ++p) v |= (unsigned long long)gacq::gen_radix_code(radix[p]) << (4 * p);
+        for (int p = 0; p < n; ++p) v |= (unsigned long long)gacq::gen_radix_code(r[p]) << (4 * p);
         return v;
     }
+    unsigned long long sched() const { return code(radix, n_pass); }
+    unsigned long long wsched() const { return code(wradix, n_wpass); }
+    unsigned qmagic() const { return W > 1 ? (unsigned)((0xffffffffull + Q) / (unsigned)Q) : 0u; }
 };
 
 bool smooth235(int64_t n) {
@@ -108,22 +114,44 @@ bool smooth235(int64_t n) {
 
 // Stockham radix schedule of an Ms-point CTA transform: radix 16 while it divides, one 8/4/2
 // pass for the remaining power of two, then the fives and threes
-void gen_passes(GenPlan& g) {
-    int m = g.Ms, e2 = 0;
+// build with -DGACQ_GEN_WS=0 to keep the CTA-wide transform in the generic correlation (A/B)
+#ifndef GACQ_GEN_WS
+#define GACQ_GEN_WS 1
+#endif
+int radix_schedule(int n, bool r25, signed char* radix) {
+    int m = n, e2 = 0, np = 0;
     while (m % 2 == 0) { m /= 2; ++e2; }
-    g.n_pass = 0;
     // 2^e2 as radix-16 passes and one 8 or 4; a lone remaining factor 2 becomes (8, 4) in
     // place of (16, 2) (the radix-2 pass is the most expensive per flop)
     int n16 = e2 / 4, rem = e2 % 4;
     if (rem == 1 && n16 > 0) { --n16; rem = 5; }
-    for (int i = 0; i < n16; ++i) g.radix[g.n_pass++] = 16;
-    if (rem == 5) { g.radix[g.n_pass++] = 8; g.radix[g.n_pass++] = 4; }
-    else if (rem) g.radix[g.n_pass++] = (signed char)(1 << rem);
+    for (int i = 0; i < n16; ++i) radix[np++] = 16;
+    if (rem == 5) { radix[np++] = 8; radix[np++] = 4; }
+    else if (rem) radix[np++] = (signed char)(1 << rem);
     // fives in pairs as radix-25 passes (5 x 5 in registers: one pass and barrier pair less)
-    // when a thread holds 32 values per pass (T = 256)
-    for (; g.T == 256 && m % 25 == 0; m /= 25) g.radix[g.n_pass++] = 25;
-    for (; m % 5 == 0; m /= 5) g.radix[g.n_pass++] = 5;
-    for (; m % 3 == 0; m /= 3) g.radix[g.n_pass++] = 3;
+    // when a thread holds 32 values per pass
+    for (; r25 && m % 25 == 0; m /= 25) radix[np++] = 25;
+    for (; m % 5 == 0; m /= 5) radix[np++] = 5;
+    for (; m % 3 == 0; m /= 3) radix[np++] = 3;
+    return np;
+}
+void gen_passes(GenPlan& g) {
+    g.n_pass = radix_schedule(g.Ms, g.T == 256, g.radix);
+    // warp split when every warp pass fits a lane's kGenWarpVpt values (Q / R groups <= 32 (VPT / R))
+    const int W = g.T / 32;
+    g.W = 1;
+    if (!GACQ_GEN_WS || g.Ms % W) return;
+    const int Q = g.Ms / W;
+    signed char wr[gacq::kGenMaxPasses];
+    const int nw = radix_schedule(Q, true, wr);
+    if (Q < 64 || Q > 32 * gacq::kGenWarpVpt) return;
+    if (g.T == 256 && 2 * (gacq::gen_smem_ws(g.Ms, Q) + 2048) > 228 * 1024) return;  // keep two CTAs per SM
+    for (int p = 0; p < nw; ++p)
+        if (Q / wr[p] > 32 * (gacq::kGenWarpVpt / wr[p])) return;
+    g.W = W;
+    g.Q = Q;
+    g.n_wpass = nw;
+    std::copy(wr, wr + nw, g.wradix);
 }
 
 void gen_threads(GenPlan& g) { g.T = 2 * (gacq::gen_smem(g.Ms) + 2048) <= 228 * 1024 ? 256 : 512; }
@@ -327,7 +355,7 @@ cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t bloc
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(T);
-    cfg.dynamicSmemBytes = gen_smem(c->gp.Ms);
+    cfg.dynamicSmemBytes = c->gp.W > 1 ? gen_smem_ws(c->gp.Ms, c->gp.Q) : gen_smem(c->gp.Ms);
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -336,6 +364,7 @@ cudaError_t launch_gen_corr_l(const gacq_ctx* c, const GenArgs& ga, int64_t bloc
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (c->gp.W > 1) return cudaLaunchKernelEx(&cfg, gacq_gen_corr_ws_kernel<L, T>, ga);
     return cudaLaunchKernelEx(&cfg, gacq_gen_corr_kernel<L, kP2, T>, ga);
 }
 cudaError_t launch_gen(const gacq_ctx* c, const GenArgs& ga, int64_t np, bool corr) {
@@ -501,7 +530,7 @@ int run_impl(gacq_ctx* c, const Input& inp, int64_t n_snap, bool per_bin, bool p
         if (profile) { CUDA_TRY(cudaEventRecord(prof_event(c, ev), c->stream)); timed.push_back({ev++, 0}); }
         GenArgs ga{(const float2*)in, in_stride, c->d_carrier, c->d_gtw, reinterpret_cast<const cx*>(c->d_gcc), Zp, c->d_rows_bin,
                    pmap, c->d_bad, p0, c->B, c->R, c->n_coh, c->P, c->n_prn, c->radius, c->gp.M, c->gp.Ms,
-                   c->gp.n_pass, c->gp.sched()};
+                   c->gp.n_pass, c->gp.sched(), c->gp.W, c->gp.Q, c->gp.n_wpass, c->gp.wsched(), c->gp.qmagic()};
         if (c->gen) {
             CUDA_TRY(launch_gen(c, ga, np, false));
         } else {
@@ -722,7 +751,9 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
                     const int L = gp.L, Ms = gp.Ms;  // residue-major (gacq_generic.cuh)
                     for (int k = 0; k < M; ++k) {
                         const auto v = std::conj(d[k]) / (double)M;
-                        gcc[(size_t)i * M + (k % L) * Ms + k / L] = make_float2((float)v.real(), (float)v.imag());
+                        const int kk = k / L;  // within the residue class; warp-split order (gen_ws_base)
+                        const int slot = gp.W > 1 ? (kk % gp.W) * gp.Q + kk / gp.W : kk;
+                        gcc[(size_t)i * M + (k % L) * Ms + slot] = make_float2((float)v.real(), (float)v.imag());
                     }
                 }
             });
@@ -780,10 +811,11 @@ int gacq_create(gacq_ctx** out, const gacq_params* p) {
         CTX_TRY(cudaMalloc(&c->d_gtw, gtw.size() * sizeof(float2)));
         CTX_TRY(cudaMemcpy(c->d_gcc, gcc.data(), gcc.size() * sizeof(float2), cudaMemcpyHostToDevice));
         CTX_TRY(cudaMemcpy(c->d_gtw, gtw.data(), gtw.size() * sizeof(float2), cudaMemcpyHostToDevice));
-        const int sm_max = gen_smem(kGenMaxMs);
+        const int sm_max = gen_smem_ws(kGenMaxMs, 32 * kGenWarpVpt);
         std::vector<const void*> ks;
 #define GACQ_GEN_KS(LL, PP, TT) \
-    ks.push_back((const void*)gacq_gen_fwd_kernel<LL, PP, TT>); ks.push_back((const void*)gacq_gen_corr_kernel<LL, PP, TT>);
+    ks.push_back((const void*)gacq_gen_fwd_kernel<LL, PP, TT>); ks.push_back((const void*)gacq_gen_corr_kernel<LL, PP, TT>); \
+    ks.push_back((const void*)gacq_gen_corr_ws_kernel<LL, TT>);
         GACQ_GEN_DISPATCH(GACQ_GEN_KS)
 #undef GACQ_GEN_KS
         for (const void* k : ks)

@@ -48,12 +48,15 @@ constexpr int kGenMaxM = kGenMaxL * kGenMaxMs;
 __host__ __device__ constexpr int gen_vpt(int T) { return kGenMaxMs / T; }
 constexpr int kGenMaxPasses = 16;  // 4-bit radix codes in a 64-bit schedule
 
+// padded transform buffer: gpad(i) < Ms + Ms / 16; the warp-split layout (gen_ws_base) needs
+// at most Ms + Ms / 16 + 16 slots
+__host__ __device__ constexpr int gen_buf(int Ms) { return Ms + Ms / 16 + 16; }
 // dynamic smem of both generic kernels: one padded CTA transform (gpad), the power accumulators
 // of the CTA's lags (<= Ms floats; shared memory rather than registers, where they would stay
 // live across the transform and spill), and the CTA transform's twiddles W_Ms^e, e < Ms, copied
 // from the plan's W_M table once per CTA (global-table reads were the top stall)
 __host__ __device__ constexpr int gen_smem(int Ms) {
-    return (int)sizeof(float2) * (Ms + Ms / 16) + (int)sizeof(float) * Ms + (int)sizeof(float2) * Ms;
+    return (int)sizeof(float2) * gen_buf(Ms) + (int)sizeof(float) * Ms + (int)sizeof(float2) * Ms;
 }
 
 // (cos, S sin)(2 pi e / T) from a full table of T entries
@@ -122,11 +125,21 @@ __device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
 // W_(Ns R)^(S k r), k = j mod Ns (Ns = product of the earlier radices), and writes
 // x[(j / Ns) Ns R + k + r Ns]. `tw` is the W_Ms table (W_(Ns R)^e = W_Ms^(e Ms / (Ns R))).
 // kLoad: the first pass (Ns = 1, no twiddles) takes its inputs from load(i) instead of x[i].
-template <int S, int R, int VPT, bool kLoad = false, class Load = int>
+// kWarp: one warp transforms x alone (lanes for threads, __syncwarp for the CTA barrier).
+// kPad: element i at i + (i >> kPad); 4 (gpad) suits the power-of-two strides, 6 the odd
+// strides of radix-25/5/3 schedules (at 625 points: 2.5x fewer excess bank wavefronts than 4;
+// no padding at all measured 6% slower, its passes spill).
+template <int S, int R, int VPT, bool kLoad = false, bool kWarp = false, int kPad = 4, class Load = int>
 __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, int Ns, const float2* __restrict__ tw,
                                                   Load&& load = 0) {
     constexpr int kGroups = VPT / R;  // groups per thread (Ms <= R kGroups blockDim)
+    const int tid = kWarp ? (int)(threadIdx.x & 31) : (int)threadIdx.x, nth = kWarp ? 32 : (int)blockDim.x;
+    auto sync = [] {
+        if constexpr (kWarp) __syncwarp();
+        else __syncthreads();
+    };
     const int ng = Ms / R, tw_step = Ms / (Ns * R);
+    auto pad = [](int i) { return i + (i >> kPad); };
     const bool pow2 = (Ns & (Ns - 1)) == 0;  // shifts, not divisions, while only radix-2^k passes preceded
     // j mod Ns otherwise by a multiply-high: floor(j m / 2^32) = floor(j / Ns) with
     // m = ceil(2^32 / Ns), exact here since j Ns < 2^26
@@ -135,14 +148,14 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
     cx v[kGroups][R];
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
-        const int j = threadIdx.x + g * blockDim.x;
+        const int j = tid + g * nth;
         if (j < ng) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if constexpr (kLoad)
                     v[g][r] = load(j + r * ng);
                 else
-                    v[g][r] = x[gpad(j + r * ng)];
+                    v[g][r] = x[pad(j + r * ng)];
             }
             if (!kLoad && Ns > 1) {
                 const int e1 = jmod(j) * tw_step;
@@ -191,18 +204,18 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
             gen_dft<S, R>(v[g]);
         }
     }
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int g = 0; g < kGroups; ++g) {
-        const int j = threadIdx.x + g * blockDim.x;
+        const int j = tid + g * nth;
         if (j < ng) {
             const int k = jmod(j);
             const int d = (j - k) * R + k;  // (j / Ns) Ns R + k
 #pragma unroll
-            for (int r = 0; r < R; ++r) x[gpad(d + r * Ns)] = v[g][r];
+            for (int r = 0; r < R; ++r) x[pad(d + r * Ns)] = v[g][r];
         }
     }
-    __syncthreads();
+    sync();
 }
 
 // Power-of-two CTA transforms (Ms = 2^logMs): the same pass with shifts for every index, radix 16
@@ -287,6 +300,11 @@ struct GenArgs {
     int M, Ms;              // transform length, points per CTA (M = L Ms)
     int n_pass;             // Stockham passes of the Ms-point CTA transform
     unsigned long long sched;  // their radices, 4 bits each from bit 0: gen_radix_code
+    // warp split (W > 1, gacq_gen_corr_ws_kernel): Ms = W Q, one Q-point transform per warp
+    // (W = warps per CTA) in n_wpass warp-local passes (wsched), then one radix-W step
+    int W, Q, n_wpass;
+    unsigned long long wsched;
+    unsigned qmagic;        // ceil(2^32 / Q): e / Q = umulhi(e, qmagic) for e < Ms
 };
 
 // 4-bit codes of the pass radices in GenArgs.sched
@@ -333,8 +351,87 @@ __device__ __forceinline__ void gen_fft_from(cx* __restrict__ x, const GenArgs& 
     }
 }
 
+// ---- warp split (gacq_gen_corr_ws_kernel) ------------------------------------------------
+// Ms = W Q: warp w transforms the Q frequencies w + W q (stored contiguously, slot w Q + q, by
+// the forward kernel and the host's code table) in its own padded sub-buffer with __syncwarp
+// only; one radix-W step across the sub-buffers then yields the Ms-point transform.
+constexpr int kGenWarpVpt = 32;  // values per lane in a warp pass (Q <= 1024)
+__host__ __device__ constexpr int gen_ws_base(int w, int Q) { return w * (Q + Q / 16 + 1); }
+// smem of the warp-split correlation: gen_smem(Ms) and the warp transforms' own W_Q table (read
+// at unit stride in their last pass; W_Ms entries e W would conflict W-fold on the banks)
+__host__ __device__ constexpr int gen_smem_ws(int Ms, int Q) { return gen_smem(Ms) + (int)sizeof(float2) * Q; }
+
+// the warp transforms' padding shift (gen_stockham_pass kPad): 4 for even Q, 6 for odd Q
+__host__ __device__ constexpr int gen_ws_pad(int Q) { return (Q & 1) ? 6 : 4; }
+__device__ __forceinline__ int gen_ws_at(int i, int shift) { return i + (i >> shift); }
+
+template <int S, int R, bool kLoad, int kPad>
+__device__ __noinline__ void gen_wpass_call(cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
+                                            const cx* __restrict__ z, const cx* __restrict__ cg) {
+    if constexpr (kLoad)
+        gen_stockham_pass<S, R, kGenWarpVpt, true, true, kPad>(
+            x, Q, 1, tw, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cg[k])); });
+    else
+        gen_stockham_pass<S, R, kGenWarpVpt, false, true, kPad>(x, Q, Ns, tw);
+}
+template <int S, bool kLoad, int kPad>
+__device__ __forceinline__ void gen_wpass_r(int R, cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
+                                            const cx* __restrict__ z, const cx* __restrict__ cg) {
+    switch (R) {
+        case 25: gen_wpass_call<S, 25, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        case 16: gen_wpass_call<S, 16, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        case 8: gen_wpass_call<S, 8, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        case 5: gen_wpass_call<S, 5, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        case 4: gen_wpass_call<S, 4, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        case 3: gen_wpass_call<S, 3, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        default: gen_wpass_call<S, 2, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+    }
+}
+template <int S, bool kLoad>
+__device__ __forceinline__ void gen_wpass(int R, cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
+                                          const cx* __restrict__ z, const cx* __restrict__ cg) {
+    if (gen_ws_pad(Q) == 4) gen_wpass_r<S, kLoad, 4>(R, x, Q, Ns, tw, z, cg);
+    else if constexpr (!kLoad) gen_wpass_r<S, false, 6>(R, x, Q, Ns, tw, z, cg);  // odd Q: staged first pass
+}
+
+// one warp: x = IDFT_Q(z . cg) (unnormalised). A power-of-two first pass reads z . cg straight
+// from global memory; a radix-25/5/3 one reads it staged through x in batches of 10 + 10 loads
+// per lane (read straight into the radix-25 pass, its 25 x 2 loads in flight spill: 5 MHz
+// correlation 15.9 ms against 12.9 staged; 8.192 MHz prefers the direct read, 28.8 against 32.1).
+__device__ __forceinline__ void gen_wfft_zc(cx* __restrict__ x, const GenArgs& a, const float2* __restrict__ tw,
+                                            const cx* __restrict__ z, const cx* __restrict__ cg) {
+    int R = gen_code_radix((int)(a.wsched & 15)), Ns = 1, p = 0;
+    if ((R & (R - 1)) == 0) {
+        gen_wpass<1, true>(R, x, a.Q, 1, tw, z, cg);
+        Ns = R;
+        p = 1;
+    } else {
+        // batches of kU loads per lane in flight (one L2 round trip per batch, not per element)
+        constexpr int kU = 10;
+        for (int i0 = threadIdx.x & 31; i0 < a.Q; i0 += 32 * kU) {
+            cx zz[kU], cc[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {  // unconditional (clamped) loads: the arrays stay in registers
+                const int i = min(i0 + 32 * u, a.Q - 1);
+                zz[u] = __ldg(&z[i]);
+                cc[u] = __ldg(&cg[i]);
+            }
+            __syncwarp();  // a scheduling fence: ptxas would otherwise pair each load with its multiply
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+                if (i0 + 32 * u < a.Q) x[gen_ws_at(i0 + 32 * u, gen_ws_pad(a.Q))] = cmul(zz[u], cc[u]);
+        }
+        __syncwarp();
+    }
+    for (; p < a.n_wpass; ++p) {
+        R = gen_code_radix((int)((a.wsched >> (4 * p)) & 15));
+        gen_wpass<1, false>(R, x, a.Q, Ns, tw, nullptr, nullptr);
+        Ns *= R;
+    }
+}
+
 // shared-memory layout of both kernels: [transform (gpad)][Ms float accumulators][Ms twiddles]
-__device__ __forceinline__ float* gen_acc(cx* sm, int Ms) { return reinterpret_cast<float*>(sm + Ms + Ms / 16); }
+__device__ __forceinline__ float* gen_acc(cx* sm, int Ms) { return reinterpret_cast<float*>(sm + gen_buf(Ms)); }
 __device__ __forceinline__ float2* gen_tws(cx* sm, int Ms) { return reinterpret_cast<float2*>(gen_acc(sm, Ms) + Ms); }
 // W_Ms^e = W_M^(e L), e < Ms, into shared memory
 __device__ __forceinline__ void gen_load_tws(float2* tws, const float2* __restrict__ tw, int Ms, int L) {
@@ -384,7 +481,101 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_fwd_kernel(GenAr
     }
     if (__syncthreads_or(fin == 0u) && threadIdx.x == 0) atomicMin(a.bad, (int)s);
     cx* dst = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
-    for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[gpad(k)];
+    if (a.W > 1) {  // warp-split order: slot w Q + q holds frequency w + W q (gacq_gen_corr_ws_kernel)
+        for (int d = threadIdx.x; d < Ms; d += blockDim.x) {
+            const int w = (int)__umulhi((unsigned)d, a.qmagic);
+            dst[d] = sm[gpad((d - w * a.Q) * a.W + w)];
+        }
+    } else {
+        for (int k = threadIdx.x; k < Ms; k += blockDim.x) dst[k] = sm[gpad(k)];
+    }
+}
+
+// first argmax (value desc, lag asc) over the cluster, then the exclusion floor
+// (acquisition.py:151-159), from the lags' accumulators accb[t - t0], t in [t0, t1); row out
+template <int L, int T>
+__device__ __forceinline__ void gen_corr_finish(const GenArgs& a, const float* accb, int t0, int t1, int lp, int pi,
+                                                int part) {
+    constexpr int kLags = kGenMaxMs / T;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ float red_v[T / 32], red_f[T / 32];
+    __shared__ int red_i[T / 32];
+    __shared__ float s_best, s_floor;
+    __shared__ int s_bidx;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    auto better = [](float v, int l, float bv, int bl) { return v > bv || (v == bv && l < bl); };
+    float best = -1.f;
+    int bidx = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kLags; ++i) {
+        const int t = t0 + threadIdx.x + i * T;
+        if (t < t1 && better(accb[t - t0], t, best, bidx)) { best = accb[t - t0]; bidx = t; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+        if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
+    }
+    if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        best = red_v[0];
+        bidx = red_i[0];
+        for (int i = 1; i < nw; ++i)
+            if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
+        s_best = best;
+        s_bidx = bidx;
+    }
+    if constexpr (L > 1) cl.sync(); else __syncthreads();
+    best = s_best;
+    bidx = s_bidx;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        if (l == part) continue;
+        const float ov = *cl.map_shared_rank(&s_best, l);
+        const int oi = *cl.map_shared_rank(&s_bidx, l);
+        if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
+    }
+    if (bidx == 0x7fffffff) { best = 0.f; bidx = 0; }  // all-NaN powers (non-finite input, flagged by K1)
+    const int64_t pair = a.pair0 + lp;
+    const int64_t s = pair / a.B;
+    const int b = (int)(pair % a.B);
+    float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
+    float fl = -1.f;
+#pragma unroll
+    for (int i = 0; i < kLags; ++i) {
+        const int t = t0 + threadIdx.x + i * T;
+        if (t < t1) {
+            int d = abs(t - bidx);
+            d = min(d, a.P - d);
+            if (d > a.radius) fl = fmaxf(fl, accb[t - t0]);  // acquisition.py:155-159
+            if (pm) pm[t] = accb[t - t0];
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
+    if (lane == 0) red_f[w] = fl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float f = red_f[0];
+        for (int i = 1; i < nw; ++i) f = fmaxf(f, red_f[i]);
+        s_floor = f;
+    }
+    if constexpr (L > 1) cl.sync(); else __syncthreads();
+    if (part == 0 && threadIdx.x == 0) {
+        float f = s_floor;
+#pragma unroll
+        for (int l = 1; l < L; ++l) f = fmaxf(f, *cl.map_shared_rank(&s_floor, l));
+        gacq_row out;
+        out.bin = b;
+        out.lag = bidx;
+        out.peak = best;
+        out.floor = f < 0.f ? 0.f : f;
+        a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
+    }
+    if constexpr (L > 1) cl.sync();  // rank 0 has read every CTA's shared memory
 }
 
 // grid: pairs_in_chunk * n_prn * L CTAs of T threads, clusters of L along x (item =
@@ -395,10 +586,6 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_kernel(GenA
     constexpr int VPT = gen_vpt(T), kLags = kGenMaxMs / T;
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) cx sm[];
-    __shared__ float red_v[T / 32], red_f[T / 32];
-    __shared__ int red_i[T / 32];
-    __shared__ float s_best, s_floor;
-    __shared__ int s_bidx;
     const int M = a.M, Ms = a.Ms;
     const int item = blockIdx.x / L, part = blockIdx.x % L;
     const int lp = item / a.n_prn, pi = item % a.n_prn;
@@ -450,80 +637,73 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_kernel(GenA
         else __syncthreads();
         // (measured: alternating two buffers to drop this barrier was no faster, at 2x the smem)
     }
-    // first argmax (value desc, lag asc) over the cluster, then the exclusion floor (acquisition.py:151-159)
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    auto better = [](float v, int l, float bv, int bl) { return v > bv || (v == bv && l < bl); };
-    float best = -1.f;
-    int bidx = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < kLags; ++i) {
-        const int t = t0 + threadIdx.x + i * T;
-        if (t < t1 && better(acc[i * T], t, best, bidx)) { best = acc[i * T]; bidx = t; }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, best, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
-        if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
-    }
-    if (lane == 0) { red_v[w] = best; red_i[w] = bidx; }
+    gen_corr_finish<L, T>(a, gen_acc(sm, Ms), t0, t1, lp, pi, part);
+}
+
+// Warp-split correlation: the grid, clusters, lag ownership and result of gacq_gen_corr_kernel,
+// with the CTA transform taken as Ms = W Q (W = T / 32 warps):
+//   F_w = IDFT_Q(Y[w + W q]) per warp (no CTA barrier inside), then for tau = t1 + Q t2
+//   E[tau] = sum_w W_W^(w t2) (W_Ms^(w t1) F_w[t1]), one radix-W step per t1 (in place: the W
+//   inputs of t1 and its W outputs share the slots (w, t1)).
+// Two CTA barriers per round instead of two per Stockham pass, and each warp's loads overlap
+// the other warps' arithmetic.
+template <int L, int T>
+__global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_ws_kernel(GenArgs a) {
+    constexpr int W = T / 32;
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) cx sm[];
+    const int M = a.M, Ms = a.Ms, Q = a.Q;
+    const int wpad = gen_ws_pad(Q);
+    const int item = blockIdx.x / L, part = blockIdx.x % L, warp = threadIdx.x >> 5;
+    const int lp = item / a.n_prn, pi = item % a.n_prn;
+    const cx* cgt = a.Cg + (int64_t)pi * M + (int64_t)part * Ms;
+    const int Pc = (a.P + L - 1) / L, t0 = part * Pc, t1 = min(a.P, t0 + Pc);
+    cg::cluster_group cl = cg::this_cluster();
+    float* accb = gen_acc(sm, Ms);  // lag t at accb[t - t0]
+    float2* tws = gen_tws(sm, Ms);
+    float2* twq = tws + Ms;  // W_Q^e = W_M^(e W L)
+    gen_load_tws(tws, a.tw, Ms, L);
+    gen_load_tws(twq, a.tw, Q, L * W);
+    for (int i = threadIdx.x; i < Ms; i += T) accb[i] = 0.f;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        best = red_v[0];
-        bidx = red_i[0];
-        for (int i = 1; i < nw; ++i)
-            if (better(red_v[i], red_i[i], best, bidx)) { best = red_v[i]; bidx = red_i[i]; }
-        s_best = best;
-        s_bidx = bidx;
-    }
-    if constexpr (L > 1) cl.sync(); else __syncthreads();
-    best = s_best;
-    bidx = s_bidx;
+    for (int rd = 0; rd < a.R; ++rd) {
+        const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
+        gen_wfft_zc(sm + gen_ws_base(warp, Q), a, twq, z + warp * Q, cgt + warp * Q);
+        __syncthreads();  // every F_w complete
+        for (int q = threadIdx.x; q < Q; q += T) {
+            cx v[W];
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        if (l == part) continue;
-        const float ov = *cl.map_shared_rank(&s_best, l);
-        const int oi = *cl.map_shared_rank(&s_bidx, l);
-        if (better(ov, oi, best, bidx)) { best = ov; bidx = oi; }
-    }
-    if (bidx == 0x7fffffff) { best = 0.f; bidx = 0; }  // all-NaN powers (non-finite input, flagged by K1)
-    const int64_t pair = a.pair0 + lp;
-    const int64_t s = pair / a.B;
-    const int b = (int)(pair % a.B);
-    float* pm = a.pmap ? a.pmap + ((int64_t)pi * a.B + b) * a.P : nullptr;
-    float fl = -1.f;
+            for (int k = 0; k < W; ++k) v[k] = sm[gen_ws_base(k, Q) + gen_ws_at(q, wpad)];
 #pragma unroll
-    for (int i = 0; i < kLags; ++i) {
-        const int t = t0 + threadIdx.x + i * T;
-        if (t < t1) {
-            int d = abs(t - bidx);
-            d = min(d, a.P - d);
-            if (d > a.radius) fl = fmaxf(fl, acc[i * T]);  // acquisition.py:155-159
-            if (pm) pm[t] = acc[i * T];
+            for (int k = 1; k < W; ++k) v[k] = cmul(v[k], gen_tw<1>(tws, k * q));
+            gen_dft<1, W>(v);
+#pragma unroll
+            for (int k = 0; k < W; ++k) {
+                if constexpr (L == 1) {
+                    const int t = q + k * Q;
+                    if (t < t1) accb[t] = fmaf(im(v[k]), im(v[k]), fmaf(re(v[k]), re(v[k]), accb[t]));  // acquisition.py:149
+                } else {
+                    sm[gen_ws_base(k, Q) + gen_ws_at(q, wpad)] = v[k];
+                }
+            }
+        }
+        if constexpr (L == 1) {
+            __syncthreads();  // the sub-buffers are read before the next round's warps overwrite them
+        } else {
+            cl.sync();  // every E_l complete
+            for (int t = t0 + threadIdx.x; t < t1; t += T) {
+                const int ee = t % Ms, qq = (int)__umulhi((unsigned)ee, a.qmagic);
+                const int e = gen_ws_base(qq, Q) + gen_ws_at(ee - qq * Q, wpad);
+                cx v = *cl.map_shared_rank(sm + e, 0);
+#pragma unroll
+                for (int l = 1; l < L; ++l)
+                    v = add2(v, cmul(*cl.map_shared_rank(sm + e, l), gen_tw<1>(a.tw, (int)(((int64_t)l * t) % M))));
+                accb[t - t0] = fmaf(im(v), im(v), fmaf(re(v), re(v), accb[t - t0]));
+            }
+            cl.sync();  // every CTA has read E_l before the next round overwrites it
         }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) fl = fmaxf(fl, __shfl_xor_sync(0xffffffffu, fl, off));
-    if (lane == 0) red_f[w] = fl;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float f = red_f[0];
-        for (int i = 1; i < nw; ++i) f = fmaxf(f, red_f[i]);
-        s_floor = f;
-    }
-    if constexpr (L > 1) cl.sync(); else __syncthreads();
-    if (part == 0 && threadIdx.x == 0) {
-        float f = s_floor;
-#pragma unroll
-        for (int l = 1; l < L; ++l) f = fmaxf(f, *cl.map_shared_rank(&s_floor, l));
-        gacq_row out;
-        out.bin = b;
-        out.lag = bidx;
-        out.peak = best;
-        out.floor = f < 0.f ? 0.f : f;
-        a.rows_bin[(s * a.n_prn + pi) * a.B + b] = out;
-    }
-    if constexpr (L > 1) cl.sync();  // rank 0 has read every CTA's shared memory
+    gen_corr_finish<L, T>(a, accb, t0, t1, lp, pi, part);
 }
 
 }  // namespace gacq
