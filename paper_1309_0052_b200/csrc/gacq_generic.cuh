@@ -355,6 +355,9 @@ __device__ __forceinline__ void gen_fft_from(cx* __restrict__ x, const GenArgs& 
 // Ms = W Q: warp w transforms the Q frequencies w + W q (stored contiguously, slot w Q + q, by
 // the forward kernel and the host's code table) in its own padded sub-buffer with __syncwarp
 // only; one radix-W step across the sub-buffers then yields the Ms-point transform.
+#ifndef GACQ_GEN_XTW
+#define GACQ_GEN_XTW 1
+#endif
 constexpr int kGenWarpVpt = 32;  // values per lane in a warp pass (Q <= 1024)
 __host__ __device__ constexpr int gen_ws_base(int w, int Q) { return w * (Q + Q / 16 + 1); }
 // smem of the warp-split correlation: gen_smem(Ms) and the warp transforms' own W_Q table (read
@@ -662,7 +665,17 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_ws_kernel(G
     float* accb = gen_acc(sm, Ms);  // lag t at accb[t - t0]
     float2* tws = gen_tws(sm, Ms);
     float2* twq = tws + Ms;  // W_Q^e = W_M^(e W L)
+#if GACQ_GEN_XTW
+    // the radix-W step's twiddles W_Ms^(k q) as a [k - 1][q] table (k < W, q < Q: (W - 1) Q < Ms
+    // entries): a warp's 32 consecutive q read it at unit stride (W_Ms^(k q) straight from the
+    // W_Ms table strided k entries: up to k-way bank conflicts for each of the W - 1 loads)
+    for (int i = threadIdx.x; i < (W - 1) * Q; i += T) {
+        const int k1 = (int)__umulhi((unsigned)i, a.qmagic), q = i - k1 * Q;
+        tws[i] = __ldg(&a.tw[(int64_t)(k1 + 1) * q * L]);
+    }
+#else
     gen_load_tws(tws, a.tw, Ms, L);
+#endif
     gen_load_tws(twq, a.tw, Q, L * W);
     for (int i = threadIdx.x; i < Ms; i += T) accb[i] = 0.f;
     __syncthreads();
@@ -675,7 +688,7 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_ws_kernel(G
 #pragma unroll
             for (int k = 0; k < W; ++k) v[k] = sm[gen_ws_base(k, Q) + gen_ws_at(q, wpad)];
 #pragma unroll
-            for (int k = 1; k < W; ++k) v[k] = cmul(v[k], gen_tw<1>(tws, k * q));
+            for (int k = 1; k < W; ++k) v[k] = cmul(v[k], gen_tw<1>(tws, GACQ_GEN_XTW ? (k - 1) * Q + q : k * q));
             gen_dft<1, W>(v);
 #pragma unroll
             for (int k = 0; k < W; ++k) {

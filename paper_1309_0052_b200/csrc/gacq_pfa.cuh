@@ -27,7 +27,12 @@ constexpr int kScr = 34;                         // K1 coop31 scratch (33 used; 
 constexpr int kSpec = 1024;                      // one spectrum in HBM and in K2's buffer: [k2][31] + 1 pad
 constexpr unsigned kSpecBytes = kSpec * sizeof(cx);
 constexpr int kXch = 1023 + 33;                  // K2 exchange [q2][31] + coop31 scratch
-constexpr int kCcHalf = 17 * 31 + 1;             // Hermitian half [k2 <= 16][31] of a conj code spectrum (+ pad)
+// Hermitian half [k2 <= 16][kCcRow] of a conj code spectrum: columns k1 < 31, and column 31 a copy
+// of column 0. Lane k1 reads the conjugate partner column 31 - k1 of rows k2 > 16 (k1 = 0 is its
+// own partner: column 31), so a half-warp's 16 reads are 16 consecutive slots: one bank wavefront
+// (with column 0 itself, lanes 0 and 1..15 hit banks 0-1 twice: 3 wavefronts instead of 2)
+constexpr int kCcRow = 32;
+constexpr int kCcHalf = 17 * kCcRow;
 constexpr int kCorrWarps = 4;                    // K2 warps per CTA (one item each)
 constexpr int kPhaseRow = 33 * 32;               // K2 scratch row of one phase: [q1 or coop slot][lane] floats
 constexpr int kTop2Row = 5 * 32;                 // K2 (kTop2) phase summary: [max, 2nd max, max index, coop 0, coop 1][lane]
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(32 * W, GACQ_FWD_MINB(D, W)) gacq_fwd_pfa_kern
 // ---- K2 ---------------------------------------------------------------------------------
 struct CorrPfaArgs {
     const cx* Z;           // spectra of this chunk, [pairs][R][D][kSpec]
-    const cx* Cc;          // [n_prn][kCcHalf] conj code spectra / 1023, rows k2 <= 16 of [k2][31]
+    const cx* Cc;          // [n_prn][kCcHalf] conj code spectra / 1023, rows k2 <= 16 of [k2][kCcRow]
     gacq_row* rows_bin;    // [n_snap][n_prn][B]
     float* pmap;           // optional [n_prn][B][P] power map (single snapshot), else null
     float* rows;           // [gridDim][kCorrWarps][D][kPhaseRow] per-phase power rows of the warp's item
@@ -382,7 +387,7 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
     cp_async_wait_all();
     __syncthreads();
     float* rows = a.rows + ((int64_t)blockIdx.x * kCorrWarps + w) * D * kPhaseRow;
-    const int pl = lane == 0 ? 0 : 31 - lane;  // Hermitian partner column of k1 = lane
+    const int pl = 31 - lane;  // Hermitian partner column of k1 = lane (31: the copy of column 0)
     const bool x0 = lane >= 1 && lane <= 16, x1 = lane >= 1 && lane <= 15;  // lanes owning coop cells
     unsigned t = 0;  // transforms of this warp: mbarrier parity t & 1
 
@@ -430,8 +435,8 @@ __global__ void __maxnreg__(GACQ_PFA_MAXNREG) gacq_corr_pfa_kernel(CorrPfaArgs a
                         dft33_stream<1>(
                             [&](int k2, int dep) {
                                 // k2 is a compile-time constant here: the branch folds away
-                                return k2 <= 16 ? cmul(Ec[k2 * 31 + dep], ccs[k2 * 31 + lane + dep])
-                                                : cmul_conj(Ec[k2 * 31 + dep], ccs[(33 - k2) * 31 + pl + dep]);
+                                return k2 <= 16 ? cmul(Ec[k2 * 31 + dep], ccs[k2 * kCcRow + lane + dep])
+                                                : cmul_conj(Ec[k2 * 31 + dep], ccs[(33 - k2) * kCcRow + pl + dep]);
                             },
                             a.zero,
                             [&]() {  // every input consumed: the buffer takes the next spectrum

@@ -53,7 +53,7 @@ __global__ void gacq_carrier_kernel(const uint64_t* __restrict__ steps, int B, i
     }
 }
 
-// Hermitian half [n_prn][17][31] (+ 1 pad) of Cc[k] = conj(DFT_1023(chip))[k] / 1023 at
+// Hermitian half [n_prn][17][kCcRow] (column 31 repeats column 0) of Cc[k] = conj(DFT_1023(chip))[k] / 1023 at
 // [k mod 33][k mod 31], k2 = k mod 33 <= 16 (gacq_pfa.cuh layout). One warp per (prn, k):
 // lanes stride the 1023 chips, float64 partial sums combined by shuffles.
 __global__ void gacq_code_spectrum_kernel(const int8_t* __restrict__ chips, int n_prn, float2* __restrict__ ccp) {
@@ -75,7 +75,12 @@ __global__ void gacq_code_spectrum_kernel(const int8_t* __restrict__ chips, int 
         re += __shfl_xor_sync(0xffffffffu, re, off);
         im += __shfl_xor_sync(0xffffffffu, im, off);
     }
-    if (lane == 0) ccp[(size_t)i * kCcHalf + (k % 33) * 31 + k % 31] = make_float2((float)(re / kChips), (float)(-im / kChips));
+    if (lane == 0) {
+        const float2 v = make_float2((float)(re / kChips), (float)(-im / kChips));
+        float2* row = ccp + (size_t)i * kCcHalf + (k % 33) * kCcRow;
+        row[k % 31] = v;
+        if (k % 31 == 0) row[31] = v;  // column 31 repeats column 0 (gacq_pfa.cuh kCcRow)
+    }
 }
 
 }  // namespace gacq
