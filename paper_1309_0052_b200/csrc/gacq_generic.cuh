@@ -139,7 +139,7 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
         else __syncthreads();
     };
     const int ng = Ms / R, tw_step = Ms / (Ns * R);
-    auto pad = [](int i) { return i + (i >> kPad); };
+    auto pad = [](int i) { return kPad ? i + (i >> kPad) : i; };
     const bool pow2 = (Ns & (Ns - 1)) == 0;  // shifts, not divisions, while only radix-2^k passes preceded
     // j mod Ns otherwise by a multiply-high: floor(j m / 2^32) = floor(j / Ns) with
     // m = ceil(2^32 / Ns), exact here since j Ns < 2^26
@@ -364,9 +364,14 @@ __host__ __device__ constexpr int gen_ws_base(int w, int Q) { return w * (Q + Q 
 // at unit stride in their last pass; W_Ms entries e W would conflict W-fold on the banks)
 __host__ __device__ constexpr int gen_smem_ws(int Ms, int Q) { return gen_smem(Ms) + (int)sizeof(float2) * Q; }
 
-// the warp transforms' padding shift (gen_stockham_pass kPad): 4 for even Q, 6 for odd Q
-__host__ __device__ constexpr int gen_ws_pad(int Q) { return (Q & 1) ? 6 : 4; }
-__device__ __forceinline__ int gen_ws_at(int i, int shift) { return i + (i >> shift); }
+// the warp transforms' padding shift (gen_stockham_pass kPad, 0 = none): 4 for even Q, 6 for odd
+// Q. At 625 points no padding at all is bank-conflict-free on every access of the 25 x 25 schedule
+// (odd store stride, unit-stride loads), yet measured 5% slower than 6 (26.2 against 24.9 ms)
+#ifndef GACQ_WS_ODD_PAD
+#define GACQ_WS_ODD_PAD 6
+#endif
+__host__ __device__ constexpr int gen_ws_pad(int Q) { return (Q & 1) ? GACQ_WS_ODD_PAD : 4; }
+__device__ __forceinline__ int gen_ws_at(int i, int shift) { return shift ? i + (i >> shift) : i; }
 
 template <int S, int R, bool kLoad, int kPad>
 __device__ __noinline__ void gen_wpass_call(cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
@@ -394,7 +399,7 @@ template <int S, bool kLoad>
 __device__ __forceinline__ void gen_wpass(int R, cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
                                           const cx* __restrict__ z, const cx* __restrict__ cg) {
     if (gen_ws_pad(Q) == 4) gen_wpass_r<S, kLoad, 4>(R, x, Q, Ns, tw, z, cg);
-    else if constexpr (!kLoad) gen_wpass_r<S, false, 6>(R, x, Q, Ns, tw, z, cg);  // odd Q: staged first pass
+    else if constexpr (!kLoad) gen_wpass_r<S, false, GACQ_WS_ODD_PAD>(R, x, Q, Ns, tw, z, cg);  // odd Q: staged first pass
 }
 
 // one warp: x = IDFT_Q(z . cg) (unnormalised). A power-of-two first pass reads z . cg straight
