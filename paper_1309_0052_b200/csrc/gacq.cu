@@ -148,6 +148,7 @@ void gen_passes(GenPlan& g) {
     if (g.T == 256 && 2 * (gacq::gen_smem_ws(g.Ms, Q) + 2048) > 228 * 1024) return;  // keep two CTAs per SM
     for (int p = 0; p < nw; ++p)
         if (Q / wr[p] > 32 * (gacq::kGenWarpVpt / wr[p])) return;
+    if (gacq::gen_ws_ptw(g.T) && gacq::gen_ptw_size(wr, nw) > Q) return;  // the warp passes' twiddle tables fit Q entries
     g.W = W;
     g.Q = Q;
     g.n_wpass = nw;

@@ -129,9 +129,11 @@ __device__ __forceinline__ int gpad(int i) { return i + (i >> 4); }
 // kPad: element i at i + (i >> kPad); 4 (gpad) suits the power-of-two strides, 6 the odd
 // strides of radix-25/5/3 schedules (at 625 points: 2.5x fewer excess bank wavefronts than 4;
 // no padding at all measured 6% slower, its passes spill).
-template <int S, int R, int VPT, bool kLoad = false, bool kWarp = false, int kPad = 4, class Load = int>
+// kPtw: the twiddle powers come from the pass's own table ptw[ci][Ns] (gen_ptw_c), read at unit stride
+template <int S, int R, int VPT, bool kLoad = false, bool kWarp = false, int kPad = 4, bool kPtw = false,
+          class Load = int>
 __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, int Ns, const float2* __restrict__ tw,
-                                                  Load&& load = 0) {
+                                                  Load&& load = 0, const float2* __restrict__ ptw = nullptr) {
     constexpr int kGroups = VPT / R;  // groups per thread (Ms <= R kGroups blockDim)
     const int tid = kWarp ? (int)(threadIdx.x & 31) : (int)threadIdx.x, nth = kWarp ? 32 : (int)blockDim.x;
     auto sync = [] {
@@ -158,18 +160,28 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
                     v[g][r] = x[pad(j + r * ng)];
             }
             if (!kLoad && Ns > 1) {
-                const int e1 = jmod(j) * tw_step;
+                const int kj = jmod(j), e1 = kj * tw_step;
+                // W^(c e1), c = gen_ptw_c(R, ci): the W_Ms table at stride c tw_step, or the pass's
+                // own table at unit stride (the same values)
+                auto twc = [&](int ci, int c) {
+                    if constexpr (kPtw) {
+                        const float2 t = ptw[ci * Ns + kj];
+                        return pk(t.x, S < 0 ? -t.y : t.y);
+                    } else {
+                        return gen_tw<S>(tw, c * e1);
+                    }
+                };
                 // W^r from the table powers W^1, W^2, W^4, W^8 and at most two products each
                 // (<= 3 roundings per twiddle): 4 loads instead of R - 1
                 cx w[R];
                 if constexpr (R == 25) {
                     // W^(5a + b) = W^(5a) W^b from the loaded 1, 2, 4, 5, 10, 20 (<= 3 roundings)
-                    w[1] = gen_tw<S>(tw, e1);
-                    w[2] = gen_tw<S>(tw, 2 * e1);
-                    w[4] = gen_tw<S>(tw, 4 * e1);
-                    w[5] = gen_tw<S>(tw, 5 * e1);
-                    w[10] = gen_tw<S>(tw, 10 * e1);
-                    w[20] = gen_tw<S>(tw, 20 * e1);
+                    w[1] = twc(0, 1);
+                    w[2] = twc(1, 2);
+                    w[4] = twc(2, 4);
+                    w[5] = twc(3, 5);
+                    w[10] = twc(4, 10);
+                    w[20] = twc(5, 20);
                     w[3] = cmul(w[1], w[2]);
                     w[15] = cmul(w[5], w[10]);
 #pragma unroll
@@ -182,10 +194,10 @@ __device__ __forceinline__ void gen_stockham_pass(cx* __restrict__ x, int Ms, in
                     gen_dft<S, R>(v[g]);
                     continue;
                 }
-                w[1] = gen_tw<S>(tw, e1);
-                if (R > 2) w[2] = gen_tw<S>(tw, 2 * e1);
-                if (R > 4 && R != 5) w[4] = gen_tw<S>(tw, 4 * e1);
-                if (R > 8) w[8] = gen_tw<S>(tw, 8 * e1);
+                w[1] = twc(0, 1);
+                if (R > 2) w[2] = twc(1, 2);
+                if (R > 4 && R != 5) w[4] = twc(2, 4);
+                if (R > 8) w[8] = twc(3, 8);
 #pragma unroll
                 for (int r = 3; r < R; ++r) {
                     if (R == 5) {  // W^3 = W^1 W^2, W^4 = W^2 W^2
@@ -358,7 +370,39 @@ __device__ __forceinline__ void gen_fft_from(cx* __restrict__ x, const GenArgs& 
 #ifndef GACQ_GEN_XTW
 #define GACQ_GEN_XTW 1
 #endif
+#ifndef GACQ_GEN_PTW
+#define GACQ_GEN_PTW 1
+#endif
+#if GACQ_GEN_PTW && !GACQ_GEN_XTW
+#error "GACQ_GEN_PTW keeps its tables in the W_Ms region GACQ_GEN_XTW leaves free"
+#endif
 constexpr int kGenWarpVpt = 32;  // values per lane in a warp pass (Q <= 1024)
+// Per-pass twiddle tables of the warp passes (GACQ_GEN_PTW): a pass of radix R after Ns points
+// loads the powers W^(c e1), e1 = (j mod Ns) tw_step, c = gen_ptw_c(R, ci), ci < gen_ptw_nc(R)
+// (gen_stockham_pass). Read from the W_Q table they stride c tw_step entries across a warp's
+// lanes: 2- to 16-way bank conflicts whenever that is even (5 MHz: c = 2, 4, 10, 20 of the
+// second radix-25 pass). The pass's table ptw[ci][k] = W_Q^(c k tw_step), k < Ns, holds the same
+// values at unit stride. All passes after the first together take sum nc(R) Ns <= Q entries
+// (checked on the host: gen_ptw_size), kept in the W_Ms region the radix-W step leaves free.
+// Radix-25 passes keep the W_Q table (nc = 0). Measured: 8.192 MHz (16, 8, 4 passes) 56.3 ->
+// 54.2 ms correlation; 5 MHz (25, 25) 24.9 -> 26.5 ms with a table for its second pass.
+__host__ __device__ constexpr int gen_ptw_nc(int R) {
+    return R == 25 ? 0 : R == 16 ? 4 : R == 8 ? 3 : (R == 4 || R == 5 || R == 3) ? 2 : 1;
+}
+__host__ __device__ constexpr int gen_ptw_c(int, int ci) { return 1 << ci; }  // W^1, W^2, W^4, W^8
+// the tables serve the 512-thread warp-split kernels only (8.192 MHz: 16 warps of 512 points,
+// passes 16, 8, 4). In the 256-thread ones (5 MHz: passes 25, 25, no table) the mere option
+// changed ptxas's register allocation of the shared pass functions: 6% slower
+__host__ __device__ constexpr bool gen_ws_ptw(int T) { return GACQ_GEN_PTW && T == 512; }
+// entries of all the tables of a warp schedule (passes 1 .. n - 1)
+__host__ __device__ inline int gen_ptw_size(const signed char* radix, int n) {
+    int Ns = n > 0 ? radix[0] : 1, t = 0;
+    for (int p = 1; p < n; ++p) {
+        t += gen_ptw_nc(radix[p]) * Ns;
+        Ns *= radix[p];
+    }
+    return t;
+}
 __host__ __device__ constexpr int gen_ws_base(int w, int Q) { return w * (Q + Q / 16 + 1); }
 // smem of the warp-split correlation: gen_smem(Ms) and the warp transforms' own W_Q table (read
 // at unit stride in their last pass; W_Ms entries e W would conflict W-fold on the banks)
@@ -373,41 +417,45 @@ __host__ __device__ constexpr int gen_smem_ws(int Ms, int Q) { return gen_smem(M
 __host__ __device__ constexpr int gen_ws_pad(int Q) { return (Q & 1) ? GACQ_WS_ODD_PAD : 4; }
 __device__ __forceinline__ int gen_ws_at(int i, int shift) { return shift ? i + (i >> shift) : i; }
 
-template <int S, int R, bool kLoad, int kPad>
+template <int S, int R, bool kLoad, int kPad, bool kPtw = false>
 __device__ __noinline__ void gen_wpass_call(cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
                                             const cx* __restrict__ z, const cx* __restrict__ cg) {
+    // (not kLoad) tw: the pass's own twiddle table with kPtw, else the W_Q table
     if constexpr (kLoad)
         gen_stockham_pass<S, R, kGenWarpVpt, true, true, kPad>(
             x, Q, 1, tw, [&](int k) { return cmul(__ldg(&z[k]), __ldg(&cg[k])); });
     else
-        gen_stockham_pass<S, R, kGenWarpVpt, false, true, kPad>(x, Q, Ns, tw);
+        gen_stockham_pass<S, R, kGenWarpVpt, false, true, kPad, kPtw>(x, Q, Ns, tw, 0, tw);
 }
-template <int S, bool kLoad, int kPad>
+template <int S, bool kLoad, int kPad, bool kPtw = false>
 __device__ __forceinline__ void gen_wpass_r(int R, cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
                                             const cx* __restrict__ z, const cx* __restrict__ cg) {
     switch (R) {
-        case 25: gen_wpass_call<S, 25, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
-        case 16: gen_wpass_call<S, 16, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
-        case 8: gen_wpass_call<S, 8, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
-        case 5: gen_wpass_call<S, 5, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
-        case 4: gen_wpass_call<S, 4, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
-        case 3: gen_wpass_call<S, 3, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
-        default: gen_wpass_call<S, 2, kLoad, kPad>(x, Q, Ns, tw, z, cg); break;
+        case 25: gen_wpass_call<S, 25, kLoad, kPad, (kPtw && gen_ptw_nc(25) > 0)>(x, Q, Ns, tw, z, cg); break;
+        case 16: gen_wpass_call<S, 16, kLoad, kPad, (kPtw && gen_ptw_nc(16) > 0)>(x, Q, Ns, tw, z, cg); break;
+        case 8: gen_wpass_call<S, 8, kLoad, kPad, (kPtw && gen_ptw_nc(8) > 0)>(x, Q, Ns, tw, z, cg); break;
+        case 5: gen_wpass_call<S, 5, kLoad, kPad, (kPtw && gen_ptw_nc(5) > 0)>(x, Q, Ns, tw, z, cg); break;
+        case 4: gen_wpass_call<S, 4, kLoad, kPad, (kPtw && gen_ptw_nc(4) > 0)>(x, Q, Ns, tw, z, cg); break;
+        case 3: gen_wpass_call<S, 3, kLoad, kPad, (kPtw && gen_ptw_nc(3) > 0)>(x, Q, Ns, tw, z, cg); break;
+        default: gen_wpass_call<S, 2, kLoad, kPad, kPtw>(x, Q, Ns, tw, z, cg); break;
     }
 }
-template <int S, bool kLoad>
+template <int S, bool kLoad, bool kPtw = false>
 __device__ __forceinline__ void gen_wpass(int R, cx* __restrict__ x, int Q, int Ns, const float2* __restrict__ tw,
                                           const cx* __restrict__ z, const cx* __restrict__ cg) {
-    if (gen_ws_pad(Q) == 4) gen_wpass_r<S, kLoad, 4>(R, x, Q, Ns, tw, z, cg);
-    else if constexpr (!kLoad) gen_wpass_r<S, false, GACQ_WS_ODD_PAD>(R, x, Q, Ns, tw, z, cg);  // odd Q: staged first pass
+    if (gen_ws_pad(Q) == 4) gen_wpass_r<S, kLoad, 4, kPtw>(R, x, Q, Ns, tw, z, cg);
+    else if constexpr (!kLoad) gen_wpass_r<S, false, GACQ_WS_ODD_PAD, kPtw>(R, x, Q, Ns, tw, z, cg);  // odd Q: staged first pass
 }
 
 // one warp: x = IDFT_Q(z . cg) (unnormalised). A power-of-two first pass reads z . cg straight
 // from global memory; a radix-25/5/3 one reads it staged through x in batches of 10 + 10 loads
 // per lane (read straight into the radix-25 pass, its 25 x 2 loads in flight spill: 5 MHz
 // correlation 15.9 ms against 12.9 staged; 8.192 MHz prefers the direct read, 28.8 against 32.1).
+// kPtw: the passes after the first read their twiddles from the tables at ptw (gen_load_ptw)
+template <bool kPtw>
 __device__ __forceinline__ void gen_wfft_zc(cx* __restrict__ x, const GenArgs& a, const float2* __restrict__ tw,
-                                            const cx* __restrict__ z, const cx* __restrict__ cg) {
+                                            const float2* __restrict__ ptw, const cx* __restrict__ z,
+                                            const cx* __restrict__ cg) {
     int R = gen_code_radix((int)(a.wsched & 15)), Ns = 1, p = 0;
     if ((R & (R - 1)) == 0) {
         gen_wpass<1, true>(R, x, a.Q, 1, tw, z, cg);
@@ -431,9 +479,34 @@ __device__ __forceinline__ void gen_wfft_zc(cx* __restrict__ x, const GenArgs& a
         }
         __syncwarp();
     }
-    for (; p < a.n_wpass; ++p) {
-        R = gen_code_radix((int)((a.wsched >> (4 * p)) & 15));
-        gen_wpass<1, false>(R, x, a.Q, Ns, tw, nullptr, nullptr);
+    if constexpr (kPtw) {
+        const float2* pt = ptw;
+        for (; p < a.n_wpass; ++p) {
+            R = gen_code_radix((int)((a.wsched >> (4 * p)) & 15));
+            gen_wpass<1, false, true>(R, x, a.Q, Ns, gen_ptw_nc(R) > 0 ? pt : tw, nullptr, nullptr);
+            if (p > 0) pt += gen_ptw_nc(R) * Ns;  // pass 0 (Ns = 1) has no twiddles and no table
+            Ns *= R;
+        }
+    } else {
+        for (; p < a.n_wpass; ++p) {
+            R = gen_code_radix((int)((a.wsched >> (4 * p)) & 15));
+            gen_wpass<1, false>(R, x, a.Q, Ns, tw, nullptr, nullptr);
+            Ns *= R;
+        }
+    }
+}
+
+// the warp passes' twiddle tables (GACQ_GEN_PTW) from the plan's W_M table: W_Q^e = W_M^(e W L)
+__device__ __forceinline__ void gen_load_ptw(float2* ptw, const GenArgs& a, int WL) {
+    int Ns = gen_code_radix((int)(a.wsched & 15));
+    for (int p = 1; p < a.n_wpass; ++p) {
+        const int R = gen_code_radix((int)((a.wsched >> (4 * p)) & 15)), tw_step = a.Q / (Ns * R);
+        const int n = gen_ptw_nc(R) * Ns;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int ci = i / Ns, k = i - ci * Ns;
+            ptw[i] = __ldg(&a.tw[(int64_t)gen_ptw_c(R, ci) * k * tw_step * WL]);
+        }
+        ptw += n;
         Ns *= R;
     }
 }
@@ -678,7 +751,10 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_ws_kernel(G
         const int k1 = (int)__umulhi((unsigned)i, a.qmagic), q = i - k1 * Q;
         tws[i] = __ldg(&a.tw[(int64_t)(k1 + 1) * q * L]);
     }
+    float2* ptw = tws + (W - 1) * Q;  // the warp passes' twiddle tables (<= Q entries, gen_ws_ptw)
+    if (gen_ws_ptw(T)) gen_load_ptw(ptw, a, L * W);
 #else
+    float2* ptw = nullptr;
     gen_load_tws(tws, a.tw, Ms, L);
 #endif
     gen_load_tws(twq, a.tw, Q, L * W);
@@ -686,7 +762,7 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_ws_kernel(G
     __syncthreads();
     for (int rd = 0; rd < a.R; ++rd) {
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
-        gen_wfft_zc(sm + gen_ws_base(warp, Q), a, twq, z + warp * Q, cgt + warp * Q);
+        gen_wfft_zc<gen_ws_ptw(T)>(sm + gen_ws_base(warp, Q), a, twq, ptw, z + warp * Q, cgt + warp * Q);
         __syncthreads();  // every F_w complete
         for (int q = threadIdx.x; q < Q; q += T) {
             cx v[W];
