@@ -65,7 +65,7 @@ CONFIGS = {
                desc="D8: the reference's default acquisition (8.184 MHz, AcqConfig(): 16 bins of 666.7 Hz, "
                     "10 x 1 ms noncoherent), 32 PRNs"),
     "g5": dict(fs=5.0e6, rounds=10, step=500.0, span_hz=5000.0, batch=64,
-               desc="G5: 10 ms snapshots @5 MHz (not chip-aligned: generic power-of-two path), 32 PRNs x 21 bins, "
+               desc="G5: 10 ms snapshots @5 MHz (not chip-aligned: generic path, native 5000-point transform), 32 PRNs x 21 bins, "
                     "10 x 1 ms noncoherent"),
     "g8": dict(fs=8.192e6, rounds=10, step=500.0, span_hz=5000.0, batch=64,
                desc="G8: 10 ms snapshots @8.192 MHz (not chip-aligned; n_coh = 8192 runs as the circular "
@@ -74,7 +74,7 @@ CONFIGS = {
 
 # dominant (K2) kernel of each device path, gacq_info.path
 KERNEL_NAMES = {2: "gacq_corr_pfa_kernel (1023-point prime-factor)",
-                4: "gacq_gen_corr_kernel (generic power-of-two path)"}
+                4: "gacq_gen_corr_ws_kernel (generic path, warp split; gacq_gen_corr_kernel where the split does not fit)"}
 
 
 def acq_kwargs(c):

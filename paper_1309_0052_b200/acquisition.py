@@ -235,7 +235,7 @@ class AcqEngine:
         """``bin_range=(b0, b1)`` searches only bins [b0, b1) of the config's grid (Doppler-bin
         sharding of one snapshot over devices); rows then carry grid-global
         bin indices, so per-shard rows merge with ``merge_bin_shards``. ``force_generic`` takes
-        the generic power-of-two path at a chip-aligned rate too (parity tests of that path)."""
+        the generic path at a chip-aligned rate too (parity tests of that path)."""
         config = config or AcqConfig()
         prns = [int(p) for p in prns]
         if not prns:

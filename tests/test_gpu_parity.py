@@ -233,7 +233,7 @@ GENERIC_ON_ALIGNED = ["c1_snap0", "c1_snap1", "c3_snap0", "coh2_snap0", "fs8_sna
 
 @pytest.mark.parametrize("name", GENERIC_ON_ALIGNED)
 def test_generic_path_on_chip_aligned_cases(pkg, name):
-    # the power-of-two path (gacq_generic.cuh) that serves rates which are not chip-aligned,
+    # the generic path (gacq_generic.cuh) that serves rates which are not chip-aligned,
     # forced onto chip-aligned golden cases: same reference answers as the 1023-point path
     c = case(name)
     eng = pkg.AcqEngine(c["fs"], c["prns"], to_cfg(pkg, c), force_generic=True)
