@@ -380,8 +380,8 @@ constexpr int kGenWarpVpt = 32;  // values per lane in a warp pass (Q <= 1024)
 // Per-pass twiddle tables of the warp passes (GACQ_GEN_PTW): a pass of radix R after Ns points
 // loads the powers W^(c e1), e1 = (j mod Ns) tw_step, c = gen_ptw_c(R, ci), ci < gen_ptw_nc(R)
 // (gen_stockham_pass). Read from the W_Q table they stride c tw_step entries across a warp's
-// lanes: 2- to 16-way bank conflicts whenever that is even (5 MHz: c = 2, 4, 10, 20 of the
-// second radix-25 pass). The pass's table ptw[ci][k] = W_Q^(c k tw_step), k < Ns, holds the same
+// lanes: 2- to 16-way bank conflicts whenever that is even (8.192 MHz, Q = 512 as 16, 8, 4: the
+// radix-8 pass strides 4, 8, 16 entries). The pass's table ptw[ci][k] = W_Q^(c k tw_step), k < Ns, holds the same
 // values at unit stride. All passes after the first together take sum nc(R) Ns <= Q entries
 // (checked on the host: gen_ptw_size), kept in the W_Ms region the radix-W step leaves free.
 // Radix-25 passes keep the W_Q table (nc = 0). Measured: 8.192 MHz (16, 8, 4 passes) 56.3 ->
