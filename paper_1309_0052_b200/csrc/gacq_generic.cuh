@@ -394,6 +394,10 @@ __host__ __device__ constexpr int gen_ptw_c(int, int ci) { return 1 << ci; }  //
 // passes 16, 8, 4). In the 256-thread ones (5 MHz: passes 25, 25, no table) the mere option
 // changed ptxas's register allocation of the shared pass functions: 6% slower
 __host__ __device__ constexpr bool gen_ws_ptw(int T) { return GACQ_GEN_PTW && T == 512; }
+// staged first-pass batch (gen_wfft_zc kU): 10 at 256 threads (20 spill: 5 MHz 25.0 -> 33.2 ms);
+// 20 at 512 threads, where ptxas's allocation of the whole kernel came out better with it (8.192
+// MHz 53.8 -> 51.4 ms, although its power-of-two first pass never runs the staged loop)
+__host__ __device__ constexpr int gen_ws_ku(int T) { return T == 512 ? 20 : 10; }
 // entries of all the tables of a warp schedule (passes 1 .. n - 1)
 __host__ __device__ inline int gen_ptw_size(const signed char* radix, int n) {
     int Ns = n > 0 ? radix[0] : 1, t = 0;
@@ -451,8 +455,9 @@ __device__ __forceinline__ void gen_wpass(int R, cx* __restrict__ x, int Q, int 
 // from global memory; a radix-25/5/3 one reads it staged through x in batches of 10 + 10 loads
 // per lane (read straight into the radix-25 pass, its 25 x 2 loads in flight spill: 5 MHz
 // correlation 15.9 ms against 12.9 staged; 8.192 MHz prefers the direct read, 28.8 against 32.1).
-// kPtw: the passes after the first read their twiddles from the tables at ptw (gen_load_ptw)
-template <bool kPtw>
+// kPtw: the passes after the first read their twiddles from the tables at ptw (gen_load_ptw);
+// kU: loads per lane in flight per batch of the staged first pass (gen_ws_ku)
+template <bool kPtw, int kU>
 __device__ __forceinline__ void gen_wfft_zc(cx* __restrict__ x, const GenArgs& a, const float2* __restrict__ tw,
                                             const float2* __restrict__ ptw, const cx* __restrict__ z,
                                             const cx* __restrict__ cg) {
@@ -463,7 +468,7 @@ __device__ __forceinline__ void gen_wfft_zc(cx* __restrict__ x, const GenArgs& a
         p = 1;
     } else {
         // batches of kU loads per lane in flight (one L2 round trip per batch, not per element)
-        constexpr int kU = 10;
+
         for (int i0 = threadIdx.x & 31; i0 < a.Q; i0 += 32 * kU) {
             cx zz[kU], cc[kU];
 #pragma unroll
@@ -762,7 +767,7 @@ __global__ void __launch_bounds__(T, T == 256 ? 2 : 1) gacq_gen_corr_ws_kernel(G
     __syncthreads();
     for (int rd = 0; rd < a.R; ++rd) {
         const cx* z = a.Z + ((int64_t)lp * a.R + rd) * M + (int64_t)part * Ms;
-        gen_wfft_zc<gen_ws_ptw(T)>(sm + gen_ws_base(warp, Q), a, twq, ptw, z + warp * Q, cgt + warp * Q);
+        gen_wfft_zc<gen_ws_ptw(T), gen_ws_ku(T)>(sm + gen_ws_base(warp, Q), a, twq, ptw, z + warp * Q, cgt + warp * Q);
         __syncthreads();  // every F_w complete
         for (int q = threadIdx.x; q < Q; q += T) {
             cx v[W];
